@@ -1,0 +1,266 @@
+/*
+ * oracle/oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, single-threaded CPU implementation (C99, IEEE double) of
+ * Takekawa's fixed-bin integration method for log K_v(x) and its derivatives
+ * (arXiv 2108.11560, /root/reference/PAPER.md, cited below as P:<line>).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` leg may load this.  The product path
+ * (paper_2108_11560_b200/) never links, imports or executes it; the two share
+ * no code, headers, helpers or constants.
+ *
+ * The algorithm is written out step by step in the paper's order and
+ * notation (Alg. 1 FindRange, Alg. 2 FindZero, Alg. 3 LogBesselK, Eq. (int)),
+ * with the readings of garbled / ambiguous passages listed in DESIGN.md §3
+ * (tags R1..R22, the same numbering as SURVEY.md §8(c)).  No blocking,
+ * fusion, recurrences or reordering: every point evaluation calls the libm
+ * routines directly.
+ *
+ * Pins (tests/test_oracle_pins.py): closed forms K_{1/2}, K_{3/2}, K_{5/2}
+ * (log K, d/dx, and d/dv at v=1/2 via e^{2x}E_1(2x)), the recurrence
+ * K_{v+1}=K_{v-1}+(2v/x)K_v, symmetry in v, the identity
+ * Eq. (deriv), d/dv = 0 at v = 0, mpmath besselk, and the
+ * independent long-double brute force in oracle/brute.c.  The plan internals
+ * (t_p, t0, t1) are "parity unpinned" by design (R20): only their sign
+ * invariants are asserted.
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#ifndef M_LN2
+#define M_LN2 0.69314718055994530942
+#endif
+
+/* FindRange doubling cap (SURVEY 8(b) constants): t <= t_s + 2^11 */
+#define ORACLE_RANGE_CAP 11
+
+typedef struct {
+    double v;   /* order, canonicalised to |v| (R15) */
+    double x;   /* argument, x > 0 */
+    double gp;  /* g(t_p), set once t_p is known */
+    double L;   /* log(eps) (R8/R9) */
+} oracle_ctx;
+
+/* log cosh(z), z >= 0, in the overflow-free form z + log1p(e^{-2z}) - log 2
+ * (a plain identity; P:91 uses log cosh). */
+static double log_cosh(double z)
+{
+    z = fabs(z);
+    return z + log1p(exp(-2.0 * z)) - M_LN2;
+}
+
+/* P:91 Eq.(3): g(t) = log cosh(vt) - x cosh t */
+static double g0(const oracle_ctx *c, double t)
+{
+    return log_cosh(c->v * t) - c->x * cosh(t);
+}
+
+/* P:95 Eq.(4): g'(t) = v tanh(vt) - x sinh t */
+static double g1(const oracle_ctx *c, double t)
+{
+    return c->v * tanh(c->v * t) - c->x * sinh(t);
+}
+
+/* P:96 Eq.(5): g''(t) = v^2 sech^2(vt) - x cosh t */
+static double g2(const oracle_ctx *c, double t)
+{
+    double ch = cosh(c->v * t);
+    return c->v * c->v / (ch * ch) - c->x * cosh(t);
+}
+
+/* threshold function of P:205: d(t) = g(t) - g(t_p) - log eps */
+static double dfun(const oracle_ctx *c, double t)
+{
+    return g0(c, t) - c->gp - c->L;
+}
+
+typedef double (*ofun)(const oracle_ctx *, double);
+
+/*
+ * Alg. 1 FindRange.  Requires F(ts) >= 0.  Finds the smallest
+ * m >= 0 with F(ts + 2^{m+1}) < 0 and returns (ts + 2^m, ts + 2^{m+1}),
+ * except that the lower end is ts itself when m = 0 (R5: t_s + 2^0 was never
+ * tested, the zero may lie in (ts, ts+1)).  Returns 0 on success, -1 when the
+ * doubling cap is exceeded.
+ */
+static int find_range(const oracle_ctx *c, ofun F, double ts, double *lo, double *hi)
+{
+    int m = 0;
+    while (F(c, ts + ldexp(1.0, m + 1)) >= 0.0) {
+        m = m + 1;
+        if (m > ORACLE_RANGE_CAP)
+            return -1;
+    }
+    *lo = (m == 0) ? ts : ts + ldexp(1.0, m);
+    *hi = ts + ldexp(1.0, m + 1);
+    return 0;
+}
+
+/*
+ * Alg. 2 FindZero, "modified Newton method", with the readings
+ * R1 (F(a) < 0 <= F(b), a is the end Alg. 3 passes first, return a),
+ * R2 (Newton from the current a), R3 (clip to the segment [a, mid]),
+ * R4 (max_iter = 10 fixed iterations when tol <= 0; tol > 0 reproduces the
+ *     literal early exit "until |a_i - a_{i-1}| < tol"),
+ * R18 (F'(a) == 0 or non-finite Newton step -> use the bisection point).
+ */
+static double find_zero(const oracle_ctx *c, ofun F, ofun dF, double a, double b,
+                        int max_iter, double tol)
+{
+    for (int i = 1; i <= max_iter; ++i) {
+        double a_prev = a;
+        double mid = a + (b - a) / 2.0;                 /* t_shrink */
+        double fa = F(c, a);
+        double dfa = dF(c, a);
+        double tn = mid;                                 /* t_newton */
+        if (dfa != 0.0) {
+            double s = a - fa / dfa;
+            if (isfinite(s))
+                tn = s;
+        }
+        double lo = fmin(a, mid), hi = fmax(a, mid);     /* Clip, R3 */
+        if (tn < lo) tn = lo;
+        if (tn > hi) tn = hi;
+        if (F(c, mid) < 0.0) {
+            a = mid;
+        } else if (F(c, tn) < 0.0) {
+            b = mid;
+            a = tn;
+        } else {
+            b = tn;
+        }
+        if (tol > 0.0 && fabs(a - a_prev) < tol)         /* literal P:197 */
+            break;
+    }
+    return a;
+}
+
+/* Integration plan of Alg. 3 for one canonical (v >= 0, x > 0). */
+static int oracle_plan(oracle_ctx *c, int max_iter, double tol,
+                       double *tp_out, double *t0_out, double *t1_out)
+{
+    double lo, hi;
+    double tp = 0.0;
+    if (c->v * c->v - c->x > 0.0) {                      /* g''(0) > 0; R17 */
+        if (find_range(c, g1, 0.0, &lo, &hi) != 0)
+            return -1;
+        tp = find_zero(c, g1, g2, hi, lo, max_iter, tol); /* P:259 (t_e, t_s) */
+    }
+    c->gp = g0(c, tp);
+    double t0 = 0.0;
+    if (-c->x - c->gp <= c->L)                           /* g(0)-g(t_p) <= log eps */
+        t0 = find_zero(c, dfun, g1, 0.0, tp, max_iter, tol);
+    if (find_range(c, dfun, tp, &lo, &hi) != 0)
+        return -1;
+    double t1 = find_zero(c, dfun, g1, hi, lo, max_iter, tol);
+    *tp_out = tp;
+    *t0_out = t0;
+    *t1_out = t1;
+    return 0;
+}
+
+/*
+ * One element.  Eq. (int) with the weights c_m multiplying the
+ * exponential (R7), the derivative integrands of Sec. 4.1
+ * d/dv f = t sinh(vt) e^{-x cosh t} = f t tanh(vt),  d/dx f = -cosh t f,
+ * accumulated over f's own range and nodes (R14).
+ *   log K = g_p + log h + log S0,  dlogK/dv = sign(v) S1/S0,  dlogK/dx = -S2/S0
+ */
+static void oracle_one(double v_in, double x, int nbins, int max_iter, double tol,
+                       double log_eps, double *logk, double *dv, double *dx,
+                       double *plan)
+{
+    double nanv = NAN;
+    if (plan) { plan[0] = plan[1] = plan[2] = plan[3] = nanv; }
+    if (!(x > 0.0) || !isfinite(x) || !isfinite(v_in)) { /* R16 */
+        *logk = *dv = *dx = nanv;
+        return;
+    }
+    double s = (v_in < 0.0) ? -1.0 : 1.0;                /* R15 */
+    oracle_ctx c = { fabs(v_in), x, 0.0, log_eps };
+    double tp, t0, t1;
+    if (oracle_plan(&c, max_iter, tol, &tp, &t0, &t1) != 0) {
+        *logk = *dv = *dx = nanv;
+        return;
+    }
+    if (plan) { plan[0] = tp; plan[1] = c.gp; plan[2] = t0; plan[3] = t1; }
+    double h = (t1 - t0) / nbins;
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+    for (int m = 0; m <= nbins; ++m) {
+        double t = t0 + m * h;
+        double cm = (m == 0 || m == nbins) ? 0.5 : 1.0;
+        double w = cm * exp(g0(&c, t) - c.gp);
+        S0 += w;
+        S1 += w * t * tanh(c.v * t);
+        S2 += w * cosh(t);
+    }
+    *logk = c.gp + log(h) + log(S0);
+    *dv = s * S1 / S0;
+    *dx = -S2 / S0;
+}
+
+/* ---------------- exported (C ABI, loaded by tests via ctypes) ------------- */
+
+/* log(2^-52): eps = DBL_EPSILON, R9 */
+double oracle_log_eps_f64(void) { return log(ldexp(1.0, -52)); }
+/* log(2^-23): eps = FLT_EPSILON, R9 */
+double oracle_log_eps_f32(void) { return log(ldexp(1.0, -23)); }
+
+/*
+ * Batched oracle.  v, x, logk, dlogk_dv, dlogk_dx: host arrays of n doubles
+ * (outputs may be NULL).  nbins >= 1 trapezoid intervals.  max_iter: FindZero
+ * iterations (paper: 10).  tol <= 0: fixed iterations (R4); tol > 0: the
+ * literal early exit.  log_eps: log of the threshold (oracle_log_eps_f64()).
+ * plan (may be NULL): 4 doubles per element (t_p, g(t_p), t0, t1).
+ * Returns 0, or -1 on invalid arguments.
+ */
+int oracle_logk(const double *v, const double *x, size_t n,
+                double *logk, double *dlogk_dv, double *dlogk_dx,
+                int nbins, int max_iter, double tol, double log_eps,
+                double *plan)
+{
+    if (nbins < 1 || max_iter < 1)
+        return -1;
+    for (size_t i = 0; i < n; ++i) {
+        double a, b, d;
+        oracle_one(v[i], x[i], nbins, max_iter, tol, log_eps, &a, &b, &d,
+                   plan ? plan + 4 * i : NULL);
+        if (logk) logk[i] = a;
+        if (dlogk_dv) dlogk_dv[i] = b;
+        if (dlogk_dx) dlogk_dx[i] = d;
+    }
+    return 0;
+}
+
+/* Point evaluations, exported so tests can check plan invariants
+ * (d(t0) <= 0, d(t1) < 0, g'(t_p) sign) without re-deriving g. */
+double oracle_g(double v, double x, double t)  { oracle_ctx c = { fabs(v), x, 0, 0 }; return g0(&c, t); }
+double oracle_g1(double v, double x, double t) { oracle_ctx c = { fabs(v), x, 0, 0 }; return g1(&c, t); }
+double oracle_g2(double v, double x, double t) { oracle_ctx c = { fabs(v), x, 0, 0 }; return g2(&c, t); }
+
+/*
+ * The LITERAL reading of Eq. (int), c_m inside the exponential:
+ *   log K ~ g_p + log sum_m h exp(c_m (g(t_m) - g_p)).
+ * Exported only so a test can show it is not the method (R7): it is off by
+ * ~1e-2 on K_{1/2}(1).
+ */
+int oracle_logk_literal_cm(const double *v, const double *x, size_t n,
+                           double *logk, int nbins, double log_eps)
+{
+    for (size_t i = 0; i < n; ++i) {
+        double plan[4], a, b, d;
+        oracle_one(v[i], x[i], nbins, 10, 0.0, log_eps, &a, &b, &d, plan);
+        if (!isfinite(a)) { logk[i] = a; continue; }
+        oracle_ctx c = { fabs(v[i]), x[i], plan[1], log_eps };
+        double t0 = plan[2], t1 = plan[3], h = (t1 - t0) / nbins, S = 0.0;
+        for (int m = 0; m <= nbins; ++m) {
+            double t = t0 + m * h;
+            double cm = (m == 0 || m == nbins) ? 0.5 : 1.0;
+            S += h * exp(cm * (g0(&c, t) - c.gp));
+        }
+        logk[i] = c.gp + log(S);
+    }
+    return 0;
+}
