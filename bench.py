@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the fused sm_100a log K_v(x) + d/dv + d/dx kernel.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--nbins 128]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference      # the CPU oracle on host cores
+
+A step is one pass of the whole hot path (range finding + fixed-bin quadrature
++ the three outputs) over one batch: config c2 of
+BASELINE.json (2^20 FP64 pairs, v~U[0,100], x~logU[0.1,1e3]) per GPU.  With
+N GPUs every rank processes its own 2^20-element batch (elements
+[r*2^20, (r+1)*2^20) of the same seeded stream): weak scaling, no collective
+on the data path; NCCL only reduces the timings (max over ranks).
+
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
+on the launching stream; between steps a 512 MiB buffer is written to flush
+L2 (outside the events).  Inputs are resident in HBM.  `e2e` repeats the
+metric through the C-ABI host-buffer entry point (pinned host arrays; H2D of
+v, x and D2H of the three outputs inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+# Per-element FP64 work of the fused kernel (DFMA counted as 2 flops, DADD/DMUL
+# as 1), measured with ncu on config c2 at nbins=128 (profiles/r01_*; DESIGN.md
+# §6).  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
+FP64_FLOPS_PER_ELEMENT = {("c2", 128): None}
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=list(workloads.CONFIGS))
+    p.add_argument("--nbins", type=int, default=128)
+    p.add_argument("--n", type=int, default=0, help="override elements per GPU")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--out", default="")
+    return p.parse_args()
+
+
+def cpu_info():
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:  # pragma: no cover
+        aff = os.cpu_count()
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return aff, model
+
+
+def oracle_rate(cfg, nbins, seconds, threads):
+    """Time the oracle (as it stands) on a bounded prefix sample of the workload."""
+    import oracle
+    v, x = workloads.generate(cfg, 0, 2048)
+    t = time.perf_counter()
+    oracle.logk(v.astype(np.float64), x.astype(np.float64), nbins, threads=threads)
+    probe = time.perf_counter() - t
+    per = probe / 2048
+    n = int(min(workloads.CONFIGS[cfg].n, max(4096, seconds / per * threads * 0.9)))
+    v, x = workloads.generate(cfg, 0, n)
+    v = v.astype(np.float64)
+    x = x.astype(np.float64)
+    t = time.perf_counter()
+    oracle.logk(v, x, nbins, threads=threads)
+    dt = time.perf_counter() - t
+    return n / dt, n, dt
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [c.strip() for c in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    cores, model = cpu_info()
+    c = workloads.CONFIGS[args.config]
+    per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    rates = []
+    n_used = 0
+    for i in range(args.warmup + args.steps):
+        r, n_used, _ = oracle_rate(args.config, args.nbins, per_step, cores)
+        if i >= args.warmup:
+            rates.append(r)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": "logK+dv+dx evals/sec FP64", "value": value,
+        "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": n_used / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if c.precision == "f64" else "f32",
+        "data": "synthetic (seeded, BASELINE.json config)",
+        "config": {"workload": args.config, "describe": c.describe, "nbins": args.nbins,
+                   "elements_per_step": n_used},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                         "sample": f"first {n_used} elements of {args.config} per step, "
+                                   f"{cores} threads, CPU {model}"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2108_11560_b200 as blk
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = workloads.CONFIGS[args.config]
+    n = args.n or c.n
+    dt = torch.float64 if c.precision == "f64" else torch.float32
+    v_np, x_np = workloads.generate(args.config, rank * n, n, n=n * world)
+    v = torch.from_numpy(v_np).to(dev)
+    x = torch.from_numpy(x_np).to(dev)
+    outs = {k: (torch.empty(n, dtype=dt, device=dev) if k in c.outputs else None)
+            for k in ("logk", "dv", "dx")}
+    fn = blk.bessel_logk_f64 if dt == torch.float64 else blk.bessel_logk_f32
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        fn(v, x, outs["logk"], outs["dv"], outs["dx"], nbins=args.nbins, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # peak-rate microbenchmarks (roofline denominators), same process and clocks
+    mb_out = torch.empty(148 * 4 * 256, dtype=torch.float64, device=dev)
+    mb_out32 = torch.empty(148 * 4 * 256, dtype=torch.float32, device=dev)
+
+    def mb(kind, out, iters):
+        blk.microbench(kind, 148 * 4, 256, 64, out, stream=stream)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ops = blk.microbench(kind, 148 * 4, 256, iters, out, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return ops / (e0.elapsed_time(e1) * 1e-3)
+
+    fp64_ops = mb("fp64", mb_out, 20000)
+    fp32_ops = mb("fp32", mb_out32, 20000)
+    mufu_ops = mb("mufu", mb_out32, 5000)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(total_ms.item())
+    ms_per_step = total_ms / args.steps
+    value = n * world * args.steps / (total_ms * 1e-3)
+
+    # end to end through the host-buffer C-ABI entry point (FP64 configs)
+    e2e = None
+    e2e_launches = 0
+    if not args.no_e2e and dt == torch.float64:
+        hv = torch.from_numpy(v_np).pin_memory()
+        hx = torch.from_numpy(x_np).pin_memory()
+        hout = {k: (torch.empty(n, dtype=dt).pin_memory() if k in c.outputs else None)
+                for k in ("logk", "dv", "dx")}
+        chunk = 1 << 18
+        ws = torch.empty(blk.host_workspace_bytes(chunk), dtype=torch.uint8, device=dev)
+
+        def hstep():
+            blk.bessel_logk_f64_host(hv, hx, hout["logk"], hout["dv"], hout["dx"],
+                                     nbins=args.nbins, workspace=ws, chunk=chunk, stream=stream)
+
+        for _ in range(2):
+            hstep()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            hstep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e_launches = args.steps * ((n + chunk - 1) // chunk)
+        e2e = {"value": n * world * args.steps / (float(e2e_ms.item()) * 1e-3), "unit": "evals/s",
+               "h2d_bytes_per_step": 2 * n * 8,
+               "d2h_bytes_per_step": len(c.outputs) * n * 8,
+               "path": "bessel_logk_f64_host (pinned host buffers, 2^18-element chunks on 3 streams)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    flops_pe = FP64_FLOPS_PER_ELEMENT.get((args.config, args.nbins))
+    if dt == torch.float64:
+        peak_meas = fp64_ops * 2 / 1e12
+        if flops_pe:
+            ach = flops_pe * n / (ms_per_step * 1e-3) / 1e12
+        else:
+            ach = None
+        roof = {"bound": "alu", "pipe": "fp64", "achieved": ach, "peak": peak_meas,
+                "unit": "TFLOP/s", "frac": (ach / peak_meas) if ach else None, "traffic": None,
+                "peak_source": "in-run DFMA microbenchmark (blk_microbench_fp64); nominal "
+                               f"{NOMINAL_FP64_TFLOPS:.1f} TF/s from 148 SM x 64 DFMA/clk x 1.965 GHz",
+                "flops_per_element": flops_pe,
+                "hbm_gbs": (n * (16 + 8 * len(c.outputs))) / (ms_per_step * 1e-3) / 1e9}
+    else:
+        roof = {"bound": "alu", "pipe": "fp32+mufu", "achieved": None,
+                "peak": fp32_ops * 2 / 1e12, "unit": "TFLOP/s", "frac": None, "traffic": None}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cores, model = cpu_info()
+        r, ns, secs = oracle_rate(args.config, args.nbins, args.cpu_seconds, cores)
+        cpu = {"value": r, "unit": "evals/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {ns} elements of {args.config} ({secs:.1f} s, {cores} threads, {model})"}
+
+    line = {
+        "metric": "logK+dv+dx evals/sec FP64" if dt == torch.float64 else "logK+dv+dx evals/sec FP32",
+        "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dt == torch.float64 else "f32",
+        "data": "synthetic (seeded numpy PCG64 blocks, BASELINE.json config distribution)",
+        "config": {"workload": args.config, "describe": c.describe, "elements_per_gpu": n,
+                   "nbins": args.nbins, "outputs": list(c.outputs),
+                   "l2": "flushed between timed steps (512 MiB write, outside events)",
+                   "parallelism": f"dp{world} (contiguous element shards, no collective)"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "gpu_launches_e2e": e2e_launches,
+        "clocks": clocks,
+        "peaks_measured": {"fp64_tflops": fp64_ops * 2 / 1e12, "fp32_tflops": fp32_ops * 2 / 1e12,
+                           "mufu_ex2_gops": mufu_ops / 1e9},
+        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+    }
+    print(json.dumps(line), flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(line, f, indent=1)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * bessel_logk.h -- C ABI of the B200 (sm_100a) fixed-bin integral method for
+ * log K_v(x) and its derivatives (Takekawa, arXiv 2108.11560).
+ *
+ * Operation (PAPER.md, cited as P:<line>):
+ *   K_v(x) = int_0^inf cosh(vt) exp(-x cosh t) dt,  v in R, x > 0   (Eq. 1-2)
+ *   For every element i the library finds the peak t_p of
+ *   g(t) = log cosh(vt) - x cosh t (t_p = 0 when v^2 <= x,
+ *   P:103-110) and the range [t0, t1] where g >= g(t_p) + log eps
+ *    with Alg. 1 FindRange and Alg. 2 FindZero (fixed
+ *   10 iterations), then integrates with a FIXED number of trapezoid
+ *   intervals n = nbins (Eq. (int)) in log-sum-exp form:
+ *     logk[i]     = log K_v(x)
+ *     dlogk_dv[i] = d log K_v(x) / dv   (integrand t sinh(vt) e^{-x cosh t})
+ *     dlogk_dx[i] = d log K_v(x) / dx   (integrand -cosh t cosh(vt) e^{-x cosh t})
+ *   The three sums share f's range and nodes (one pass).
+ *
+ * Conventions shared by every entry point
+ *   - v, x, logk, dlogk_dv, dlogk_dx of the device entry points are DEVICE
+ *     pointers to n contiguous elements, owned by the caller.  The library
+ *     never allocates, frees or synchronises on those paths; the call enqueues
+ *     one kernel on `stream` (NULL = legacy default stream) and returns.
+ *   - Any of logk / dlogk_dv / dlogk_dx may be NULL to skip that output (a
+ *     compile-time kernel variant; skipped outputs cost nothing and do not
+ *     change the others bit-wise).  At least one must be non-NULL.  Outputs
+ *     must not alias the inputs or each other.
+ *   - Per-element domain (never fails the batch): x <= 0, x or v NaN/inf ->
+ *     all requested outputs NaN.  v < 0 -> evaluated at |v| with dlogk_dv
+ *     negated (K is even in v).  The FindRange doubling cap (t <= t_s + 2^12)
+ *     exceeded -> NaN.
+ *   - Results are a pure function of (v[i], x[i], nbins, entry point,
+ *     options): bit-identical across runs, batch permutations, shard counts
+ *     and output subsets.
+ *   - Reentrant and thread-safe; no global mutable state except the one-time
+ *     lazily created helper streams of the *_host entry points.
+ *
+ * Errors: BLK_EINVAL (no CUDA call made) when n > 0 and v or x is NULL, all
+ * outputs are NULL, nbins < 2 or nbins > BLK_MAX_NBINS, or an option is out of
+ * range; n == 0 is a no-op returning BLK_OK.  BLK_ECUDA when a CUDA call or the
+ * kernel launch fails (message via bessel_logk_last_error()).
+ */
+#ifndef BESSEL_LOGK_H
+#define BESSEL_LOGK_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BLK_API __attribute__((visibility("default")))
+#else
+#define BLK_API
+#endif
+
+/* Same type as the CUDA runtime's cudaStream_t (an opaque CUstream handle). */
+struct CUstream_st;
+typedef struct CUstream_st *cudaStream_t;
+
+typedef enum {
+    BLK_OK = 0,
+    BLK_EINVAL = 1,
+    BLK_ECUDA = 2
+} blk_status;
+
+/* Largest accepted nbins (the paper fixes none). */
+#define BLK_MAX_NBINS 65536
+
+/* Range-finding precision (options.range_mode). */
+#define BLK_RANGE_AUTO 0  /* FP32 (FMA + MUFU pipes) inside its safe domain, else FP64 */
+#define BLK_RANGE_F64 1   /* working-precision range finding, as the paper does */
+
+typedef struct {
+    /* Lanes cooperating on one element (1 = one element per thread; 2..32,
+     * a power of two, splits the n+1 bins across lanes with a warp-shuffle
+     * reduction).  0 = automatic choice from n (documented in DESIGN.md). */
+    int lanes_per_element;
+    /* BLK_RANGE_AUTO or BLK_RANGE_F64. */
+    int range_mode;
+    /* Threads per block (0 = default 128; else a multiple of 32 in [32, 1024]). */
+    int block_threads;
+} blk_options;
+
+/*
+ * FP64 entry point.  eps = 2^-52 (log eps = -36.0437, R9).
+ * v, x: device, n doubles each.  logk, dlogk_dv, dlogk_dx: device, n doubles
+ * each, or NULL.  nbins: number of trapezoid INTERVALS n (n+1 nodes).
+ */
+BLK_API blk_status bessel_logk_f64(const double *v, const double *x, size_t n,
+                           double *logk, double *dlogk_dv, double *dlogk_dx,
+                           int nbins, cudaStream_t stream);
+
+/* FP32 entry point: same contract, float arrays, eps = 2^-23. */
+BLK_API blk_status bessel_logk_f32(const float *v, const float *x, size_t n,
+                           float *logk, float *dlogk_dv, float *dlogk_dx,
+                           int nbins, cudaStream_t stream);
+
+/* Same as above with explicit options (opts may be NULL = all defaults). */
+BLK_API blk_status bessel_logk_f64_ex(const double *v, const double *x, size_t n,
+                              double *logk, double *dlogk_dv, double *dlogk_dx,
+                              int nbins, const blk_options *opts,
+                              cudaStream_t stream);
+BLK_API blk_status bessel_logk_f32_ex(const float *v, const float *x, size_t n,
+                              float *logk, float *dlogk_dv, float *dlogk_dx,
+                              int nbins, const blk_options *opts,
+                              cudaStream_t stream);
+
+/*
+ * Host-buffer entry point (end-to-end use).  v, x, logk, dlogk_dv, dlogk_dx
+ * are HOST pointers (page-locked memory overlaps copies with compute;
+ * pageable memory works but serialises).  The batch is split into chunks of
+ * `chunk` elements (0 = default 2^20) that are copied host->device, computed
+ * and copied device->host on a small pool of streams so that transfers of one
+ * chunk overlap the kernel of another.  workspace: DEVICE buffer of at least
+ * bessel_logk_host_workspace_bytes(chunk, 8) bytes, owned by the caller.
+ * Blocking: returns after all results are in host memory (the work is ordered
+ * after prior work on `stream`).
+ */
+BLK_API size_t bessel_logk_host_workspace_bytes(size_t chunk, size_t elem_bytes);
+BLK_API blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n,
+                                double *logk, double *dlogk_dv, double *dlogk_dx,
+                                int nbins, void *workspace, size_t workspace_bytes,
+                                size_t chunk, cudaStream_t stream);
+
+/* Human-readable message for the last non-OK status on this thread. */
+BLK_API const char *bessel_logk_last_error(void);
+
+/* Library version string. */
+BLK_API const char *bessel_logk_version(void);
+
+/*
+ * Peak-rate microbenchmarks used as the roofline denominators (bench.py):
+ * each thread runs `iters` iterations of BLK_MB_UNROLL instructions spread
+ * over 8 independent dependency chains; out (device, blocks*threads
+ * elements) receives a data-dependent value so the work cannot be elided.
+ *   ops = blocks * threads * iters * BLK_MB_UNROLL
+ *   fp64: DFMA (2 flops each); fp32: FFMA (2 flops each); mufu: MUFU.EX2
+ */
+#define BLK_MB_UNROLL 16
+BLK_API blk_status blk_microbench_fp64(int blocks, int threads, int iters, double *out,
+                               cudaStream_t stream);
+BLK_API blk_status blk_microbench_fp32(int blocks, int threads, int iters, float *out,
+                               cudaStream_t stream);
+BLK_API blk_status blk_microbench_mufu(int blocks, int threads, int iters, float *out,
+                               cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BESSEL_LOGK_H */

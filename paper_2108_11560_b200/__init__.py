@@ -1,0 +1,205 @@
+"""B200-native (sm_100a) batched log K_v(x), d/dv and d/dx by Takekawa's
+fixed-bin integral method (arXiv 2108.11560).
+
+Thin ctypes binding over ``libbessel_logk.so`` (C ABI in
+``include/bessel_logk.h``).  Argument marshalling only: every step of the
+method runs in the CUDA kernels.  PyTorch provides device memory and streams.
+There is no CPU fallback: if the shared library is missing the import of the
+native handle raises.
+
+    import torch, paper_2108_11560_b200 as blk
+    v = torch.rand(1 << 20, dtype=torch.float64, device="cuda") * 100
+    x = torch.rand(1 << 20, dtype=torch.float64, device="cuda") * 10 + 0.1
+    logk, dv, dx = blk.log_bessel_k(v, x, nbins=128)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+__all__ = [
+    "BLK_OK", "BLK_EINVAL", "BLK_ECUDA", "BLK_RANGE_AUTO", "BLK_RANGE_F64",
+    "BesselLogKError", "lib", "library_path", "header_functions",
+    "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
+    "host_workspace_bytes", "microbench", "DEFAULT_NBINS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+library_path = os.path.join(_HERE, "libbessel_logk.so")
+HEADER = os.path.join(_ROOT, "include", "bessel_logk.h")
+
+BLK_OK, BLK_EINVAL, BLK_ECUDA = 0, 1, 2
+BLK_RANGE_AUTO, BLK_RANGE_F64 = 0, 1
+BLK_MB_UNROLL = 16
+# Trapezoid intervals used when the caller gives none (the paper states no n,
+# P:222; R10).
+DEFAULT_NBINS = 128
+
+
+class BesselLogKError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"bessel_logk status {status}: {msg}")
+        self.status = status
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("lanes_per_element", ctypes.c_int), ("range_mode", ctypes.c_int),
+                ("block_threads", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded native library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(library_path):
+            raise ImportError(
+                f"{library_path} not found: build it with "
+                "`python -m paper_2108_11560_b200.build` (no CPU fallback exists)")
+        L = ctypes.CDLL(library_path)
+        vp, sz, ci = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+        for name in ("bessel_logk_f64", "bessel_logk_f32"):
+            f = getattr(L, name)
+            f.restype = ci
+            f.argtypes = [vp, vp, sz, vp, vp, vp, ci, vp]
+        for name in ("bessel_logk_f64_ex", "bessel_logk_f32_ex"):
+            f = getattr(L, name)
+            f.restype = ci
+            f.argtypes = [vp, vp, sz, vp, vp, vp, ci, ctypes.POINTER(_Options), vp]
+        L.bessel_logk_host_workspace_bytes.restype = sz
+        L.bessel_logk_host_workspace_bytes.argtypes = [sz, sz]
+        L.bessel_logk_f64_host.restype = ci
+        L.bessel_logk_f64_host.argtypes = [vp, vp, sz, vp, vp, vp, ci, vp, sz, sz, vp]
+        L.bessel_logk_last_error.restype = ctypes.c_char_p
+        L.bessel_logk_version.restype = ctypes.c_char_p
+        for name in ("blk_microbench_fp64", "blk_microbench_fp32", "blk_microbench_mufu"):
+            f = getattr(L, name)
+            f.restype = ci
+            f.argtypes = [ci, ci, ci, vp, vp]
+        _lib = L
+    return _lib
+
+
+def header_functions():
+    """Names of every function declared in include/bessel_logk.h."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"BLK_API\s+[\w\s\*]+?\b(\w+)\s*\(", txt)))
+
+
+def _check(st):
+    if st != BLK_OK:
+        raise BesselLogKError(st, lib().bessel_logk_last_error().decode())
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev_ptr(t, dtype, n, name):
+    import torch
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous() or t.numel() != n:
+        raise ValueError(f"{name} must be contiguous with {n} elements")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _opts(lanes_per_element, range_mode, block_threads):
+    if lanes_per_element == 0 and range_mode == 0 and block_threads == 0:
+        return None
+    return _Options(int(lanes_per_element), int(range_mode), int(block_threads))
+
+
+def _call(prec, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element,
+          range_mode, block_threads):
+    import torch
+    dtype = torch.float64 if prec == 64 else torch.float32
+    n = v.numel()
+    pv = _dev_ptr(v, dtype, n, "v")
+    px = _dev_ptr(x, dtype, n, "x")
+    po = [_dev_ptr(t, dtype, n, nm) for t, nm in
+          ((logk, "logk"), (dlogk_dv, "dlogk_dv"), (dlogk_dx, "dlogk_dx"))]
+    L = lib()
+    o = _opts(lanes_per_element, range_mode, block_threads)
+    s = _stream_handle(stream)
+    if o is None:
+        f = L.bessel_logk_f64 if prec == 64 else L.bessel_logk_f32
+        _check(f(pv, px, n, po[0], po[1], po[2], int(nbins), s))
+    else:
+        f = L.bessel_logk_f64_ex if prec == 64 else L.bessel_logk_f32_ex
+        _check(f(pv, px, n, po[0], po[1], po[2], int(nbins), ctypes.byref(o), s))
+
+
+def bessel_logk_f64(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
+                    stream=None, lanes_per_element=0, range_mode=BLK_RANGE_AUTO,
+                    block_threads=0):
+    """Enqueue the FP64 kernel on ``stream`` writing into the given float64 CUDA tensors."""
+    _call(64, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element,
+          range_mode, block_threads)
+
+
+def bessel_logk_f32(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
+                    stream=None, lanes_per_element=0, range_mode=BLK_RANGE_AUTO,
+                    block_threads=0):
+    """Enqueue the FP32 kernel on ``stream`` writing into the given float32 CUDA tensors."""
+    _call(32, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element,
+          range_mode, block_threads)
+
+
+def log_bessel_k(v, x, nbins=DEFAULT_NBINS, outputs=("logk", "dv", "dx"), **kw):
+    """Allocate outputs and evaluate; returns a tuple in the order of ``outputs``."""
+    import torch
+    dt = v.dtype
+    if dt not in (torch.float64, torch.float32):
+        raise TypeError("v must be float64 or float32")
+    want = {k: (torch.empty_like(v) if k in outputs else None) for k in ("logk", "dv", "dx")}
+    f = bessel_logk_f64 if dt == torch.float64 else bessel_logk_f32
+    f(v, x.to(dt).contiguous(), want["logk"], want["dv"], want["dx"], nbins=nbins, **kw)
+    return tuple(want[k] for k in outputs)
+
+
+def host_workspace_bytes(chunk=0, elem_bytes=8):
+    return lib().bessel_logk_host_workspace_bytes(int(chunk), int(elem_bytes))
+
+
+def bessel_logk_f64_host(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
+                         workspace=None, chunk=0, stream=None):
+    """Host-buffer entry point: v, x, outputs are CPU float64 tensors (pinned for overlap);
+    ``workspace`` a CUDA uint8 tensor of >= host_workspace_bytes(chunk) bytes."""
+    import torch
+    n = v.numel()
+
+    def hp(t, name):
+        if t is None:
+            return None
+        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != n:
+            raise TypeError(f"{name} must be a contiguous CPU float64 tensor of {n} elements")
+        return ctypes.c_void_p(t.data_ptr())
+
+    if workspace is None or not workspace.is_cuda:
+        raise TypeError("workspace must be a CUDA tensor")
+    _check(lib().bessel_logk_f64_host(
+        hp(v, "v"), hp(x, "x"), n, hp(logk, "logk"), hp(dlogk_dv, "dlogk_dv"),
+        hp(dlogk_dx, "dlogk_dx"), int(nbins), ctypes.c_void_p(workspace.data_ptr()),
+        workspace.numel() * workspace.element_size(), int(chunk), _stream_handle(stream)))
+
+
+def microbench(kind, blocks, threads, iters, out, stream=None):
+    """Enqueue a peak-rate microbenchmark ('fp64' DFMA, 'fp32' FFMA, 'mufu' EX2).
+    Returns the instruction count it executes."""
+    f = {"fp64": lib().blk_microbench_fp64, "fp32": lib().blk_microbench_fp32,
+         "mufu": lib().blk_microbench_mufu}[kind]
+    _check(f(int(blocks), int(threads), int(iters), ctypes.c_void_p(out.data_ptr()),
+             _stream_handle(stream)))
+    return blocks * threads * iters * BLK_MB_UNROLL

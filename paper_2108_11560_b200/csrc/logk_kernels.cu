@@ -1,0 +1,436 @@
+// logk_kernels.cu -- fused sm_100a kernels and the C ABI (include/bessel_logk.h).
+//
+// One kernel per precision does the whole hot path for its elements
+// (SURVEY.md §8(a) a1-a7): load + canonicalise, regime test, peak, t0, t1
+// (logk_range.cuh), fixed-bin quadrature with the three sums
+// (logk_quad.cuh), epilogue log/divide, store.  No shared state besides the
+// 2 KB exp table per block; no atomics.  LPE (lanes per element) > 1 splits
+// the n+1 nodes of one element across LPE adjacent lanes (every lane derives
+// the identical plan) and combines the sums with warp shuffles.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/bessel_logk.h"
+#include "logk_quad.cuh"
+#include "logk_range.cuh"
+
+namespace blk {
+
+constexpr int kDefaultThreads = 128;
+
+template <int LPE, class T>
+__device__ __forceinline__ T group_sum(T a) {
+#pragma unroll
+  for (int o = 1; o < LPE; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
+
+// Bins [mb, me) handled by lane `sub` of LPE lanes for n+1 nodes.
+template <int LPE>
+__device__ __forceinline__ void lane_bins(int n, int sub, int &mb, int &me) {
+  const int per = (n + 1 + LPE - 1) / LPE;
+  mb = min(sub * per, n + 1);
+  me = min(mb + per, n + 1);
+}
+
+template <bool LOGK, bool DV, bool DX, int LPE>
+__global__ void __launch_bounds__(128)
+logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
+                double *__restrict__ logk, double *__restrict__ dlogk_dv,
+                double *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  __shared__ double tab[kExpTab];
+  fill_exp_table(tab);
+  __syncthreads();
+
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = gtid / LPE;
+  const int sub = (int)(gtid % LPE);
+  const bool live = i < n_el;
+  // Lanes past the end still take part in the shuffles (full-warp masks).
+  const double vraw = live ? vin[i] : 1.0;
+  const double x = live ? xin[i] : 1.0;
+  const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
+  const double v = fabs(vraw);
+  const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
+
+  double t0 = 0.0, t1 = 0.0, gp = 0.0;
+  bool ok = false;
+  if (valid) {
+    if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
+      float tp32, gp32, t032, t132;
+      ok = make_plan<MathF32>(v, x, kLogEpsF64, tp32, gp32, t032, t132);
+      t0 = t032; t1 = t132; gp = gp32;
+    } else {
+      double tp64;
+      ok = make_plan<MathF64>(v, x, kLogEpsF64, tp64, gp, t0, t1);
+    }
+    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+  }
+  Sums64 s{0.0, 0.0, 0.0};
+  const double h = (t1 - t0) / nbins;
+  if (ok) {
+    int mb, me;
+    lane_bins<LPE>(nbins, sub, mb, me);
+    s = quad_f64<DV, DX>(v, x, t0, h, gp, nbins, mb, me, tab);
+  }
+  if (LPE > 1) {
+    s.S0 = group_sum<LPE>(s.S0);
+    if (DV) s.S1 = group_sum<LPE>(s.S1);
+    if (DX) s.S2 = group_sum<LPE>(s.S2);
+  }
+  if (!live || sub != 0) return;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
+  if (LOGK) logk[i] = ok ? gp + log(h) + log(s.S0) : nanv;
+  if (DV) dlogk_dv[i] = ok ? sgn * (s.S1 / s.S0) : nanv;
+  if (DX) dlogk_dx[i] = ok ? -(s.S2 / s.S0) : nanv;
+}
+
+template <bool LOGK, bool DV, bool DX, int LPE>
+__global__ void __launch_bounds__(128)
+logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, size_t n_el,
+                float *__restrict__ logk, float *__restrict__ dlogk_dv,
+                float *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = gtid / LPE;
+  const int sub = (int)(gtid % LPE);
+  const bool live = i < n_el;
+  const float vraw = live ? vin[i] : 1.0f;
+  const float x = live ? xin[i] : 1.0f;
+  const bool valid = (x > 0.0f) && isfinite(x) && isfinite(vraw);
+  const float v = fabsf(vraw);
+  const float sgn = (vraw < 0.0f) ? -1.0f : 1.0f;
+
+  float t0 = 0.0f, t1 = 0.0f, gp = 0.0f;
+  bool ok = false;
+  if (valid) {
+    if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
+      float tp;
+      ok = make_plan<MathF32>(v, x, kLogEpsF32, tp, gp, t0, t1);
+    } else {
+      double tp64, gp64, t064, t164;
+      ok = make_plan<MathF64>(v, x, kLogEpsF32, tp64, gp64, t064, t164);
+      t0 = (float)t064; t1 = (float)t164; gp = (float)gp64;
+    }
+    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+  }
+  Sums32 s{0.0f, 0.0f, 0.0f};
+  const float h = (t1 - t0) / nbins;
+  if (ok) {
+    int mb, me;
+    lane_bins<LPE>(nbins, sub, mb, me);
+    s = quad_f32<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
+  }
+  if (LPE > 1) {
+    s.S0 = group_sum<LPE>(s.S0);
+    if (DV) s.S1 = group_sum<LPE>(s.S1);
+    if (DX) s.S2 = group_sum<LPE>(s.S2);
+  }
+  if (!live || sub != 0) return;
+  const float nanv = __int_as_float(0x7fc00000);
+  if (LOGK) logk[i] = ok ? gp + logf(h) + logf(s.S0) : nanv;
+  if (DV) dlogk_dv[i] = ok ? sgn * __fdiv_rn(s.S1, s.S0) : nanv;
+  if (DX) dlogk_dx[i] = ok ? -__fdiv_rn(s.S2, s.S0) : nanv;
+}
+
+// ------------------------------------------------------------ microbenchmarks
+constexpr int kMbChains = 8;
+
+__global__ void mb_fp64_kernel(int iters, double *out) {
+  double a[kMbChains];
+  const double m = 1.0 + 1e-9 * threadIdx.x, c = 1e-12;
+#pragma unroll
+  for (int j = 0; j < kMbChains; ++j) a[j] = 1.0 + j * 1e-3 + blockIdx.x * 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < BLK_MB_UNROLL / kMbChains; ++u) {
+#pragma unroll
+      for (int j = 0; j < kMbChains; ++j) a[j] = fma(a[j], m, c);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < kMbChains; ++j) s += a[j];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void mb_fp32_kernel(int iters, float *out) {
+  float a[kMbChains];
+  const float m = 1.0f + 1e-7f * threadIdx.x, c = 1e-9f;
+#pragma unroll
+  for (int j = 0; j < kMbChains; ++j) a[j] = 1.0f + j * 1e-3f + blockIdx.x * 1e-6f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < BLK_MB_UNROLL / kMbChains; ++u) {
+#pragma unroll
+      for (int j = 0; j < kMbChains; ++j) a[j] = fmaf(a[j], m, c);
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int j = 0; j < kMbChains; ++j) s += a[j];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void mb_mufu_kernel(int iters, float *out) {
+  float a[kMbChains];
+#pragma unroll
+  for (int j = 0; j < kMbChains; ++j) a[j] = -1e-3f * (j + 1) - 1e-9f * threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < BLK_MB_UNROLL / kMbChains; ++u) {
+#pragma unroll
+      for (int j = 0; j < kMbChains; ++j) a[j] = ex2_approx(a[j]) - 1.0f;
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int j = 0; j < kMbChains; ++j) s += a[j];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+}  // namespace blk
+
+// ===================================================================== C ABI
+namespace {
+
+thread_local char g_err[256] = "";
+
+blk_status fail(blk_status st, const char *msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return st;
+}
+
+blk_status cuda_fail(cudaError_t e, const char *where) {
+  snprintf(g_err, sizeof g_err, "%s: %s", where, cudaGetErrorString(e));
+  return BLK_ECUDA;
+}
+
+int auto_lanes(size_t n, int nbins) {
+  // One element per thread fills the chip once n >= ~148 SMs x 512 threads;
+  // below that, split the bins of each element over a few lanes.
+  const size_t fill = (size_t)148 * 512;
+  int lanes = 1;
+  while (lanes < 32 && n * lanes < fill && (nbins + 1) / (lanes * 2) >= 8) lanes *= 2;
+  return lanes;
+}
+
+template <class T>
+blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void *o2,
+                    const void *o3, int nbins, const blk_options *opts, int &lanes,
+                    int &mode, int &threads) {
+  lanes = 0; mode = BLK_RANGE_AUTO; threads = blk::kDefaultThreads;
+  if (opts) {
+    lanes = opts->lanes_per_element;
+    mode = opts->range_mode;
+    if (opts->block_threads) threads = opts->block_threads;
+  }
+  if (nbins < 2 || nbins > BLK_MAX_NBINS) return fail(BLK_EINVAL, "nbins out of range [2, 65536]");
+  if (!o1 && !o2 && !o3) return fail(BLK_EINVAL, "all outputs are NULL");
+  if (n > 0 && (!v || !x)) return fail(BLK_EINVAL, "v or x is NULL");
+  if (mode != BLK_RANGE_AUTO && mode != BLK_RANGE_F64) return fail(BLK_EINVAL, "bad range_mode");
+  if (lanes < 0 || lanes > 32 || (lanes & (lanes - 1))) return fail(BLK_EINVAL, "lanes_per_element must be 0 or a power of two <= 32");
+  if (threads < 32 || threads > 128 || threads % 32) return fail(BLK_EINVAL, "block_threads must be a multiple of 32 in [32, 128]");
+  if (n > ((size_t)1 << 40)) return fail(BLK_EINVAL, "n too large");
+  if (lanes == 0) lanes = auto_lanes(n, nbins);
+  return BLK_OK;
+}
+
+template <class K, class T>
+blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, const T *v,
+                    const T *x, T *a, T *b, T *c, int nbins, int mode) {
+  const size_t total = n * (size_t)lanes;
+  const size_t blocks = (total + threads - 1) / threads;
+  if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "grid too large");
+  kern<<<(unsigned)blocks, threads, 0, st>>>(v, x, n, a, b, c, nbins, mode);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return BLK_OK;
+}
+
+#define BLK_DISPATCH_LPE(KER, L, O1, O2, O3)                                        \
+  switch (L) {                                                                      \
+    case 1: return launch_k(KER<O1, O2, O3, 1>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+    case 2: return launch_k(KER<O1, O2, O3, 2>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+    case 4: return launch_k(KER<O1, O2, O3, 4>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+    case 8: return launch_k(KER<O1, O2, O3, 8>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+    case 16: return launch_k(KER<O1, O2, O3, 16>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+    default: return launch_k(KER<O1, O2, O3, 32>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+  }
+
+template <class T>
+blk_status run(const T *v, const T *x, size_t n, T *a, T *b, T *c, int nbins,
+               const blk_options *opts, cudaStream_t stream) {
+  int lanes, mode, th;
+  blk_status st = validate(v, x, n, a, b, c, nbins, opts, lanes, mode, th);
+  if (st != BLK_OK) return st;
+  if (n == 0) return BLK_OK;
+  const int sel = (a ? 4 : 0) | (b ? 2 : 0) | (c ? 1 : 0);
+  if constexpr (sizeof(T) == 8) {
+    switch (sel) {
+      case 7: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, true, true)
+      case 6: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, true, false)
+      case 5: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, false, true)
+      case 4: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, false, false)
+      case 3: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, false, true, true)
+      case 2: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, false, true, false)
+      default: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, false, false, true)
+    }
+  } else {
+    switch (sel) {
+      case 7: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, true, true, true)
+      case 6: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, true, true, false)
+      case 5: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, true, false, true)
+      case 4: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, true, false, false)
+      case 3: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, false, true, true)
+      case 2: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, false, true, false)
+      default: BLK_DISPATCH_LPE(blk::logk_f32_kernel, lanes, false, false, true)
+    }
+  }
+}
+
+// ---- host-buffer pipeline
+constexpr int kHostStreams = 3;
+std::mutex g_pool_mu;
+struct Pool {
+  int device = -1;
+  cudaStream_t s[kHostStreams];
+  cudaEvent_t ev[kHostStreams];
+};
+Pool g_pools[64];
+
+blk_status get_pool(Pool *&out) {
+  int dev;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(BLK_ECUDA, "device ordinal out of range");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  Pool &p = g_pools[dev];
+  if (p.device < 0) {
+    for (int k = 0; k < kHostStreams; ++k) {
+      e = cudaStreamCreateWithFlags(&p.s[k], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+      e = cudaEventCreateWithFlags(&p.ev[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+    }
+    p.device = dev;
+  }
+  out = &p;
+  return BLK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *bessel_logk_last_error(void) { return g_err; }
+const char *bessel_logk_version(void) { return "bessel_logk 0.1.0 sm_100a"; }
+
+blk_status bessel_logk_f64(const double *v, const double *x, size_t n, double *logk,
+                           double *dlogk_dv, double *dlogk_dx, int nbins, cudaStream_t stream) {
+  return run<double>(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, nullptr, stream);
+}
+blk_status bessel_logk_f32(const float *v, const float *x, size_t n, float *logk,
+                           float *dlogk_dv, float *dlogk_dx, int nbins, cudaStream_t stream) {
+  return run<float>(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, nullptr, stream);
+}
+blk_status bessel_logk_f64_ex(const double *v, const double *x, size_t n, double *logk,
+                              double *dlogk_dv, double *dlogk_dx, int nbins,
+                              const blk_options *opts, cudaStream_t stream) {
+  return run<double>(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, opts, stream);
+}
+blk_status bessel_logk_f32_ex(const float *v, const float *x, size_t n, float *logk,
+                              float *dlogk_dv, float *dlogk_dx, int nbins,
+                              const blk_options *opts, cudaStream_t stream) {
+  return run<float>(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, opts, stream);
+}
+
+size_t bessel_logk_host_workspace_bytes(size_t chunk, size_t elem_bytes) {
+  if (chunk == 0) chunk = (size_t)1 << 20;
+  // per helper stream: v, x and three outputs of `chunk` elements, 256-B aligned
+  const size_t arr = ((chunk * elem_bytes) + 255) / 256 * 256;
+  return (size_t)kHostStreams * 5 * arr;
+}
+
+blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, double *logk,
+                                double *dlogk_dv, double *dlogk_dx, int nbins, void *workspace,
+                                size_t workspace_bytes, size_t chunk, cudaStream_t stream) {
+  int lanes, mode, th;
+  blk_status st = validate(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, nullptr, lanes, mode, th);
+  if (st != BLK_OK) return st;
+  if (n == 0) return BLK_OK;
+  if (chunk == 0) chunk = (size_t)1 << 20;
+  if (!workspace || workspace_bytes < bessel_logk_host_workspace_bytes(chunk, 8))
+    return fail(BLK_EINVAL, "workspace missing or too small");
+  Pool *pool;
+  st = get_pool(pool);
+  if (st != BLK_OK) return st;
+  const size_t arr = ((chunk * 8) + 255) / 256 * 256;
+  cudaError_t e;
+  // order after the caller's prior work
+  cudaEvent_t start_ev;
+  if ((e = cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming)) != cudaSuccess)
+    return cuda_fail(e, "cudaEventCreate");
+  cudaEventRecord(start_ev, stream);
+  for (int k = 0; k < kHostStreams; ++k) cudaStreamWaitEvent(pool->s[k], start_ev, 0);
+  size_t nchunks = (n + chunk - 1) / chunk;
+  for (size_t c = 0; c < nchunks; ++c) {
+    const int k = (int)(c % kHostStreams);
+    cudaStream_t s = pool->s[k];
+    char *base = (char *)workspace + (size_t)k * 5 * arr;
+    double *dv_ = (double *)(base), *dx_ = (double *)(base + arr);
+    double *o0 = (double *)(base + 2 * arr), *o1 = (double *)(base + 3 * arr),
+           *o2 = (double *)(base + 4 * arr);
+    const size_t off = c * chunk, m = (n - off < chunk) ? n - off : chunk;
+    const size_t bytes = m * 8;
+    if ((e = cudaMemcpyAsync(dv_, v + off, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "H2D v");
+    if ((e = cudaMemcpyAsync(dx_, x + off, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "H2D x");
+    blk_options o{lanes, mode, th};
+    st = run<double>(dv_, dx_, m, logk ? o0 : nullptr, dlogk_dv ? o1 : nullptr,
+                     dlogk_dx ? o2 : nullptr, nbins, &o, s);
+    if (st != BLK_OK) return st;
+    if (logk && (e = cudaMemcpyAsync(logk + off, o0, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e, "D2H logk");
+    if (dlogk_dv && (e = cudaMemcpyAsync(dlogk_dv + off, o1, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e, "D2H dv");
+    if (dlogk_dx && (e = cudaMemcpyAsync(dlogk_dx + off, o2, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e, "D2H dx");
+  }
+  for (int k = 0; k < kHostStreams; ++k) {
+    cudaEventRecord(pool->ev[k], pool->s[k]);
+    cudaStreamWaitEvent(stream, pool->ev[k], 0);
+  }
+  cudaEventDestroy(start_ev);
+  if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "synchronize");
+  return BLK_OK;
+}
+
+blk_status blk_microbench_fp64(int blocks, int threads, int iters, double *out, cudaStream_t s) {
+  if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out)
+    return fail(BLK_EINVAL, "bad microbench args");
+  blk::mb_fp64_kernel<<<blocks, threads, 0, s>>>(iters, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "mb_fp64");
+}
+blk_status blk_microbench_fp32(int blocks, int threads, int iters, float *out, cudaStream_t s) {
+  if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out)
+    return fail(BLK_EINVAL, "bad microbench args");
+  blk::mb_fp32_kernel<<<blocks, threads, 0, s>>>(iters, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "mb_fp32");
+}
+blk_status blk_microbench_mufu(int blocks, int threads, int iters, float *out, cudaStream_t s) {
+  if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out)
+    return fail(BLK_EINVAL, "bad microbench args");
+  blk::mb_mufu_kernel<<<blocks, threads, 0, s>>>(iters, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "mb_mufu");
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+"""Parity helpers: GPU results vs the CPU oracle (tolerances from BASELINE.json
+north_star: relative 1e-12 on log K and 1e-10 on the derivatives in FP64,
+1e-5 / 1e-4 in FP32).  log K is compared relative to max(1, |ref|) (DESIGN.md
+R19: log K crosses 0); a derivative whose oracle value is exactly 0 (v = 0)
+must be exactly 0 on the GPU too."""
+import numpy as np
+
+TOL = {
+    "f64": {"logk": 1e-12, "dv": 1e-10, "dx": 1e-10},
+    "f32": {"logk": 1e-5, "dv": 1e-4, "dx": 1e-4},
+}
+
+
+def errors(got, ref, kind):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if kind == "logk":
+        return np.abs(got - ref) / np.maximum(1.0, np.abs(ref))
+    err = np.abs(got - ref) / np.where(ref == 0, 1.0, np.abs(ref))
+    return np.where(ref == 0, np.where(got == 0, 0.0, np.inf), err)
+
+
+def assert_parity(got: dict, ref: dict, prec: str, ctx: str = ""):
+    """got/ref: dicts kind -> array.  NaN positions must agree."""
+    for kind, g in got.items():
+        r = ref[kind]
+        g = np.asarray(g, dtype=np.float64)
+        r = np.asarray(r, dtype=np.float64)
+        nan_g, nan_r = np.isnan(g), np.isnan(r)
+        assert np.array_equal(nan_g, nan_r), f"{ctx} {kind}: NaN mismatch at {np.nonzero(nan_g != nan_r)[0][:10]}"
+        ok = ~nan_r
+        e = errors(g[ok], r[ok], kind)
+        if e.size:
+            worst = int(np.argmax(e))
+            assert e[worst] <= TOL[prec][kind], (
+                f"{ctx} {kind}: max rel err {e[worst]:.3e} > {TOL[prec][kind]:.0e} "
+                f"(got {g[ok][worst]!r}, ref {r[ok][worst]!r}, local index {worst})")
+
+
+def max_errors(got: dict, ref: dict):
+    out = {}
+    for kind, g in got.items():
+        r = np.asarray(ref[kind], dtype=np.float64)
+        ok = ~np.isnan(r)
+        e = errors(np.asarray(g, dtype=np.float64)[ok], r[ok], kind)
+        out[kind] = float(e.max()) if e.size else 0.0
+    return out

@@ -1,0 +1,245 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU oracle,
+element by element on the same seeded inputs (BASELINE.json configs c1-c5),
+plus edge cases, invariances and full-size sampled checks in the launch
+configuration bench.py times."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2108_11560_b200 as blk
+import workloads
+from parity import assert_parity, max_errors
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+NB = 128
+KINDS = ("logk", "dv", "dx")
+
+
+def run_gpu(v, x, nbins=NB, outputs=KINDS, **kw):
+    dt = torch.float32 if v.dtype == np.float32 else torch.float64
+    vt = torch.from_numpy(np.ascontiguousarray(v)).to(DEV, dt)
+    xt = torch.from_numpy(np.ascontiguousarray(x)).to(DEV, dt)
+    res = blk.log_bessel_k(vt, xt, nbins=nbins, outputs=outputs, **kw)
+    torch.cuda.synchronize()
+    return {k: r.cpu().numpy() for k, r in zip(outputs, res)}
+
+
+def run_oracle(v, x, nbins=NB, threads=8):
+    r = oracle.logk(np.asarray(v, np.float64), np.asarray(x, np.float64), nbins, threads=threads)
+    return dict(zip(KINDS, r))
+
+
+# --------------------------------------------------------------- per config
+MID_N = 3 * 8192 + 77   # many blocks of 128 threads and a ragged tail
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_parity_config(cfg):
+    c = workloads.CONFIGS[cfg]
+    n = min(c.n, MID_N)
+    v, x = workloads.generate(cfg, 0, n)
+    outs = c.outputs
+    got = run_gpu(v, x, outputs=outs)
+    ref = run_oracle(v, x)
+    assert_parity(got, ref, c.precision, cfg)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_parity_config_f64_range(cfg):
+    """range_mode=BLK_RANGE_F64: the paper's working-precision range finder."""
+    c = workloads.CONFIGS[cfg]
+    v, x = workloads.generate(cfg, 0, 4099)
+    got = run_gpu(v, x, outputs=c.outputs, range_mode=blk.BLK_RANGE_F64)
+    assert_parity(got, run_oracle(v, x), c.precision, cfg)
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 4, 8, 16, 32])
+def test_parity_lanes_per_element(lanes):
+    """K3: bins split across lanes + shuffle reduction, same tolerance."""
+    v, x = workloads.generate("c2", 0, 3001)
+    got = run_gpu(v, x, lanes_per_element=lanes)
+    assert_parity(got, run_oracle(v, x), "f64", f"lanes={lanes}")
+    got32 = run_gpu(v.astype(np.float32), x.astype(np.float32), lanes_per_element=lanes)
+    assert_parity(got32, run_oracle(v.astype(np.float32), x.astype(np.float32)), "f32",
+                  f"f32 lanes={lanes}")
+
+
+@pytest.mark.parametrize("nbins", [2, 3, 16, 48, 64, 127, 256, 1000])
+def test_parity_nbins(nbins):
+    v, x = workloads.generate("c1", 0, 1500)
+    got = run_gpu(v, x, nbins=nbins)
+    ref = run_oracle(v, x, nbins=nbins)
+    if nbins >= 48:
+        assert_parity(got, ref, "f64", f"nbins={nbins}")
+    else:
+        # coarse grids: both sides follow the same trapezoid, but with ranges
+        # found in different precisions the discretisation error itself
+        # (up to ~1e-1 at n=2) differs; require agreement to 10% of it.
+        brute = dict(zip(KINDS, oracle.brute(v, x, threads=8)))
+        for k in KINDS:
+            disc = np.abs(ref[k] - brute[k])
+            assert np.all(np.abs(got[k] - ref[k]) <= 0.1 * disc + 1e-12 * np.maximum(1, np.abs(ref[k]))), k
+
+
+def test_max_nbins():
+    v, x = workloads.generate("c3", 0, 300)
+    got = run_gpu(v, x, nbins=65536)
+    ref = run_oracle(v, x, nbins=65536)
+    assert_parity(got, ref, "f64", "nbins=65536")
+
+
+# ------------------------------------------------------------------ edges
+def test_empty_and_tiny_batches():
+    for n in (0, 1, 2, 31, 32, 33, 127, 129):
+        v, x = workloads.generate("c2", 5, n)
+        got = run_gpu(v, x)
+        if n:
+            assert_parity(got, run_oracle(v, x), "f64", f"n={n}")
+        else:
+            assert all(g.size == 0 for g in got.values())
+
+
+def test_special_values():
+    v = np.array([0.0, -0.0, 0.5, -0.5, -3.7, 2.5, 1.0, 1.0, 1.0, np.nan, np.inf, 1.0, 1.0, 0.1])
+    x = np.array([1.0, 2.0, 1.0, 1.0, 0.3, 3.0, 0.0, -1.0, np.nan, 1.0, 1.0, np.inf, 1e-3, 0.01])
+    got = run_gpu(v, x)
+    ref = run_oracle(v, x)
+    assert_parity(got, ref, "f64", "special")
+    assert got["dv"][0] == 0.0 and got["dv"][1] == 0.0
+    # exact closed form at v=1/2 (DLMF 10.39.2)
+    assert abs(got["logk"][2] - (0.5 * np.log(np.pi / 2) - 1)) < 1e-13
+    assert abs(got["dx"][2] + 1.5) < 1e-13
+    # odd/even in v
+    assert got["logk"][2] == got["logk"][3] and got["dv"][2] == -got["dv"][3]
+
+
+def test_extreme_domain():
+    """Beyond the paper's grid (R22), incl. the FP64 range-finder fallback domain."""
+    v = np.array([0, 0, 5, 0, 10, 2000, 5000, 1e4, 0.5, 5, 0, 30.0, 2e4, 3.0])
+    x = np.array([1e3, 1e4, 1e5, 1e6, 1e8, 1e-3, 1e-4, 1e-2, 1e-6, 1e-10, 1e-8, 1e-30, 1.0, 1e-40])
+    got = run_gpu(v, x)
+    ref = run_oracle(v, x)
+    e = max_errors(got, ref)
+    assert e["logk"] <= 1e-12 and e["dx"] <= 1e-10 and e["dv"] <= 1e-10, e
+
+
+def test_misaligned_pointers():
+    """torch storage offsets can leave 8-B (not 16-B) alignment."""
+    v, x = workloads.generate("c2", 0, 1001)
+    vt = torch.from_numpy(v).to(DEV)
+    xt = torch.from_numpy(x).to(DEV)
+    base = torch.empty(3 * 1001 + 3, dtype=torch.float64, device=DEV)
+    out = [base[1:1002], base[1002:2003], base[2003:3004]]
+    blk.bessel_logk_f64(vt[1:], xt[1:], out[0][1:], out[1][1:], out[2][1:], nbins=NB)
+    torch.cuda.synchronize()
+    got = {k: o[1:].cpu().numpy() for k, o in zip(KINDS, out)}
+    assert_parity(got, run_oracle(v[1:], x[1:]), "f64", "misaligned")
+
+
+# ------------------------------------------------------------ invariances
+def test_bitwise_determinism_and_output_subsets():
+    v, x = workloads.generate("c2", 0, 5000)
+    a = run_gpu(v, x)
+    b = run_gpu(v, x)
+    for k in KINDS:
+        assert np.array_equal(a[k], b[k])
+    for subset in (("logk",), ("dv",), ("dx",), ("logk", "dx"), ("dv", "dx")):
+        s = run_gpu(v, x, outputs=subset)
+        for k in subset:
+            assert np.array_equal(s[k], a[k]), (subset, k)
+
+
+def test_permutation_and_shard_invariance():
+    v, x = workloads.generate("c3", 0, 4096)
+    a = run_gpu(v, x, lanes_per_element=1)
+    perm = np.random.default_rng(0).permutation(v.size)
+    b = run_gpu(v[perm], x[perm], lanes_per_element=1)
+    for k in KINDS:
+        assert np.array_equal(a[k][perm], b[k])
+    for p in (2, 4, 8):
+        bounds = np.linspace(0, v.size, p + 1).astype(int)
+        parts = [run_gpu(v[lo:hi], x[lo:hi], lanes_per_element=1) for lo, hi in zip(bounds[:-1], bounds[1:])]
+        for k in KINDS:
+            assert np.array_equal(np.concatenate([q[k] for q in parts]), a[k])
+
+
+def test_host_entry_point_matches_device_path():
+    v, x = workloads.generate("c2", 0, 70001)
+    dev = run_gpu(v, x, lanes_per_element=1)
+    vt = torch.from_numpy(v).pin_memory()
+    xt = torch.from_numpy(x).pin_memory()
+    outs = [torch.empty(v.size, dtype=torch.float64).pin_memory() for _ in range(3)]
+    chunk = 16384
+    ws = torch.empty(blk.host_workspace_bytes(chunk), dtype=torch.uint8, device=DEV)
+    blk.bessel_logk_f64_host(vt, xt, *outs, nbins=NB, workspace=ws, chunk=chunk)
+    for k, o in zip(KINDS, outs):
+        assert np.array_equal(o.numpy(), dev[k]), k
+
+
+def test_mathematical_properties_gpu():
+    """Symmetry, recurrence and Eq. (deriv) hold on the GPU outputs directly."""
+    rng = np.random.default_rng(2)
+    v = rng.uniform(1.0, 60.0, 3000)
+    x = 10 ** rng.uniform(-2, 2.5, 3000)
+    lm = run_gpu(v - 1, x)["logk"]
+    a = run_gpu(v, x)
+    lp = run_gpu(v + 1, x)["logk"]
+    rec_l = np.exp(lp - a["logk"])
+    rec_r = np.exp(lm - a["logk"]) + 2 * v / x
+    assert np.max(np.abs(rec_l - rec_r) / rec_r) < 1e-11
+    ref_dx = -(np.exp(lm - a["logk"]) + np.exp(lp - a["logk"])) / 2
+    assert np.max(np.abs(a["dx"] - ref_dx) / np.abs(ref_dx)) < 1e-11
+    neg = run_gpu(-v, x)
+    assert np.array_equal(neg["logk"], a["logk"]) and np.array_equal(neg["dv"], -a["dv"])
+
+
+# ----------------------------------------------- full sizes, bench launch cfg
+def _full_check(cfg, n_sample=2048, edge=512, chunked=False):
+    c = workloads.CONFIGS[cfg]
+    n = c.n
+    dt = torch.float32 if c.precision == "f32" else torch.float64
+    vt = torch.empty(n, dtype=dt, device=DEV)
+    xt = torch.empty(n, dtype=dt, device=DEV)
+    step = 1 << 24
+    for s in range(0, n, step):
+        v, x = workloads.generate(cfg, s, min(step, n - s))
+        vt[s:s + v.size] = torch.from_numpy(v).to(DEV)
+        xt[s:s + v.size] = torch.from_numpy(x).to(DEV)
+    res = blk.log_bessel_k(vt, xt, nbins=NB, outputs=c.outputs)
+    torch.cuda.synchronize()
+    idx = np.unique(np.concatenate([workloads.sample_indices(cfg, n_sample, seed=11),
+                                    np.arange(edge), np.arange(n - edge, n)]))
+    it = torch.from_numpy(idx).to(DEV)
+    got = {k: r[it].cpu().numpy() for k, r in zip(c.outputs, res)}
+    vs, xs = workloads.gather(cfg, idx)
+    ref = run_oracle(vs, xs)
+    assert_parity(got, ref, c.precision, f"{cfg} full")
+    # properties at every element: finite, dlogK/dx <= -1, dlogK/dv >= 0 (v >= 0)
+    for k, r in zip(c.outputs, res):
+        assert bool(torch.isfinite(r).all()), k
+        if k == "dx":
+            assert float(r.max()) <= -1.0 + (1e-5 if dt == torch.float32 else 1e-12)
+        if k == "dv":
+            assert float(r.min()) >= 0.0
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_full_size_sampled(cfg):
+    _full_check(cfg)
+
+
+def test_full_size_c5_sampled():
+    _full_check("c5", n_sample=1024, edge=256)
+
+
+def test_microbenchmarks_run():
+    out = torch.empty(148 * 256, dtype=torch.float64, device=DEV)
+    ops = blk.microbench("fp64", 148, 256, 10, out)
+    out32 = torch.empty(148 * 256, dtype=torch.float32, device=DEV)
+    blk.microbench("fp32", 148, 256, 10, out32)
+    blk.microbench("mufu", 148, 256, 10, out32)
+    torch.cuda.synchronize()
+    assert ops == 148 * 256 * 10 * 16
+    assert bool(torch.isfinite(out).all())
