@@ -34,9 +34,10 @@
  *   - Reentrant and thread-safe; no global mutable state except the one-time
  *     lazily created helper streams of the *_host entry points.
  *
- * Errors: BLK_EINVAL (no CUDA call made) when n > 0 and v or x is NULL, all
- * outputs are NULL, nbins < 2 or nbins > BLK_MAX_NBINS, or an option is out of
- * range; n == 0 is a no-op returning BLK_OK.  BLK_ECUDA when a CUDA call or the
+ * Errors: BLK_EINVAL (no CUDA call made) when nbins < 2 or nbins >
+ * BLK_MAX_NBINS, an option is out of range, or n > 0 and v or x is NULL or all
+ * outputs are NULL; otherwise n == 0 is a no-op returning BLK_OK (pointers are
+ * not inspected).  BLK_ECUDA when a CUDA call or the
  * kernel launch fails (message via bessel_logk_last_error()).
  */
 #ifndef BESSEL_LOGK_H

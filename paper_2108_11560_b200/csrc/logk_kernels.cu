@@ -230,7 +230,7 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
     if (opts->block_threads) threads = opts->block_threads;
   }
   if (nbins < 2 || nbins > BLK_MAX_NBINS) return fail(BLK_EINVAL, "nbins out of range [2, 65536]");
-  if (!o1 && !o2 && !o3) return fail(BLK_EINVAL, "all outputs are NULL");
+  if (n > 0 && !o1 && !o2 && !o3) return fail(BLK_EINVAL, "all outputs are NULL");
   if (n > 0 && (!v || !x)) return fail(BLK_EINVAL, "v or x is NULL");
   if (mode != BLK_RANGE_AUTO && mode != BLK_RANGE_F64) return fail(BLK_EINVAL, "bad range_mode");
   if (lanes < 0 || lanes > 32 || (lanes & (lanes - 1))) return fail(BLK_EINVAL, "lanes_per_element must be 0 or a power of two <= 32");

@@ -14,7 +14,8 @@ implements the five BASELINE.json configs (recipe in DESIGN.md §4):
 fixed blocks of 2^20 elements; block b of config k is drawn from
 numpy PCG64(SeedSequence(seed, spawn_key=(k, b))), arrays in the order v, x
 (c5: v, a, d, y).  Element i of a config is therefore the same no matter
-how the batch is sharded across ranks or sampled for the oracle.
+how the batch is sharded across ranks or sampled for the oracle, and of the
+total size requested (blocks are always drawn at full length and sliced).
 """
 from __future__ import annotations
 
@@ -98,7 +99,7 @@ def generate(name: str, start: int = 0, count: int | None = None, seed: int = 0,
     b0, b1 = start // BLOCK, (start + count + BLOCK - 1) // BLOCK
     for b in range(b0, b1):
         blk_len = min(BLOCK, total - b * BLOCK)
-        v, x = _block(cfg, b, blk_len, seed)
+        v, x = _block(cfg, b, BLOCK, seed)
         lo = max(start, b * BLOCK) - b * BLOCK
         hi = min(start + count, b * BLOCK + blk_len) - b * BLOCK
         vs.append(v[lo:hi])
@@ -128,8 +129,7 @@ def gather(name: str, idx, seed: int = 0, n: int | None = None):
     blocks = idx // BLOCK
     for b in np.unique(blocks):
         sel = np.nonzero(blocks == b)[0]
-        blk_len = min(BLOCK, total - int(b) * BLOCK)
-        vb, xb = _block(cfg, int(b), blk_len, seed)
+        vb, xb = _block(cfg, int(b), BLOCK, seed)
         v[sel] = vb[idx[sel] - b * BLOCK]
         x[sel] = xb[idx[sel] - b * BLOCK]
     dt = np.float32 if cfg.precision == "f32" else np.float64
