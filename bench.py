@@ -39,7 +39,10 @@ import workloads  # noqa: E402
 # Per-element FP64 work of the fused kernel (DFMA counted as 2 flops, DADD/DMUL
 # as 1), measured with ncu on config c2 at nbins=128 (profiles/r01_*; DESIGN.md
 # §6).  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
-FP64_FLOPS_PER_ELEMENT = {("c2", 128): None}
+FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4654.3}
+# dram__bytes_read.sum + dram__bytes_write.sum of one launch (same capture),
+# per element; the outputs stay in L2 until after the kernel.
+DRAM_BYTES_PER_ELEMENT = {("c2", 128): 16.07}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
 
 
@@ -301,8 +304,11 @@ def main():
             ach = flops_pe * n / (ms_per_step * 1e-3) / 1e12
         else:
             ach = None
+        dbe = DRAM_BYTES_PER_ELEMENT.get((args.config, args.nbins))
         roof = {"bound": "alu", "pipe": "fp64", "achieved": ach, "peak": peak_meas,
-                "unit": "TFLOP/s", "frac": (ach / peak_meas) if ach else None, "traffic": None,
+                "unit": "TFLOP/s", "frac": (ach / peak_meas) if ach else None,
+                "traffic": (dbe * n) if dbe else None, "traffic_unit": "bytes per launch (ncu)",
+                "algorithmic_bytes": n * (16 + 8 * len(c.outputs)),
                 "peak_source": "in-run DFMA microbenchmark (blk_microbench_fp64); nominal "
                                f"{NOMINAL_FP64_TFLOPS:.1f} TF/s from 148 SM x 64 DFMA/clk x 1.965 GHz",
                 "flops_per_element": flops_pe,

@@ -79,9 +79,21 @@ typedef struct {
     int lanes_per_element;
     /* BLK_RANGE_AUTO or BLK_RANGE_F64. */
     int range_mode;
-    /* Threads per block (0 = default 128; else a multiple of 32 in [32, 1024]). */
+    /* Threads per block of the simple kernel (0 = default 128; else a
+     * multiple of 32 in [32, 128]). */
     int block_threads;
+    /* Kernel variant: BLK_KERNEL_AUTO (= BLK_KERNEL_SIMPLE),
+     * BLK_KERNEL_SIMPLE (one element -- or lanes_per_element lanes -- per
+     * thread, both phases in every warp), BLK_KERNEL_WS (FP64 only,
+     * persistent: producer warps find the ranges, consumer warps integrate;
+     * one element per lane).  Every variant gives bit-identical results for
+     * lanes_per_element = 1. */
+    int kernel;
 } blk_options;
+
+#define BLK_KERNEL_AUTO 0
+#define BLK_KERNEL_SIMPLE 1
+#define BLK_KERNEL_WS 2
 
 /*
  * FP64 entry point.  eps = 2^-52 (log eps = -36.0437, R9).
@@ -116,13 +128,27 @@ BLK_API blk_status bessel_logk_f32_ex(const float *v, const float *x, size_t n,
  * chunk overlap the kernel of another.  workspace: DEVICE buffer of at least
  * bessel_logk_host_workspace_bytes(chunk, 8) bytes, owned by the caller.
  * Blocking: returns after all results are in host memory (the work is ordered
- * after prior work on `stream`).
+ * after prior work on `stream`).  Every chunk runs the simple kernel with one
+ * element per lane, so results equal bessel_logk_f64_ex with
+ * lanes_per_element = 1 bit for bit, whatever the chunking.
  */
 BLK_API size_t bessel_logk_host_workspace_bytes(size_t chunk, size_t elem_bytes);
 BLK_API blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n,
                                 double *logk, double *dlogk_dv, double *dlogk_dx,
                                 int nbins, void *workspace, size_t workspace_bytes,
                                 size_t chunk, cudaStream_t stream);
+
+/*
+ * Diagnostic entry point: the FP64 hot path as two kernels -- `phases` bit 0
+ * runs the range finding for all elements into `scratch` (DEVICE, 32 bytes
+ * per element, caller-owned), bit 1 the quadrature + epilogue from it.  All
+ * three outputs are required.  Results equal bessel_logk_f64 bit for bit; it
+ * exists to time the two phases separately (tools/, profiles/).
+ */
+BLK_API blk_status blk_debug_split_f64(const double *v, const double *x, size_t n,
+                                       double *logk, double *dlogk_dv, double *dlogk_dx,
+                                       int nbins, void *scratch, int phases,
+                                       cudaStream_t stream);
 
 /* Human-readable message for the last non-OK status on this thread. */
 BLK_API const char *bessel_logk_last_error(void);

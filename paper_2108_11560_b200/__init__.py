@@ -20,6 +20,7 @@ import re
 
 __all__ = [
     "BLK_OK", "BLK_EINVAL", "BLK_ECUDA", "BLK_RANGE_AUTO", "BLK_RANGE_F64",
+    "BLK_KERNEL_AUTO", "BLK_KERNEL_SIMPLE", "BLK_KERNEL_WS",
     "BesselLogKError", "lib", "library_path", "header_functions",
     "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
     "host_workspace_bytes", "microbench", "DEFAULT_NBINS",
@@ -32,6 +33,7 @@ HEADER = os.path.join(_ROOT, "include", "bessel_logk.h")
 
 BLK_OK, BLK_EINVAL, BLK_ECUDA = 0, 1, 2
 BLK_RANGE_AUTO, BLK_RANGE_F64 = 0, 1
+BLK_KERNEL_AUTO, BLK_KERNEL_SIMPLE, BLK_KERNEL_WS = 0, 1, 2
 BLK_MB_UNROLL = 16
 # Trapezoid intervals used when the caller gives none (the paper states no n,
 # P:222; R10).
@@ -46,7 +48,7 @@ class BesselLogKError(RuntimeError):
 
 class _Options(ctypes.Structure):
     _fields_ = [("lanes_per_element", ctypes.c_int), ("range_mode", ctypes.c_int),
-                ("block_threads", ctypes.c_int)]
+                ("block_threads", ctypes.c_int), ("kernel", ctypes.c_int)]
 
 
 _lib = None
@@ -115,14 +117,14 @@ def _dev_ptr(t, dtype, n, name):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _opts(lanes_per_element, range_mode, block_threads):
-    if lanes_per_element == 0 and range_mode == 0 and block_threads == 0:
+def _opts(lanes_per_element, range_mode, block_threads, kernel):
+    if lanes_per_element == 0 and range_mode == 0 and block_threads == 0 and kernel == 0:
         return None
-    return _Options(int(lanes_per_element), int(range_mode), int(block_threads))
+    return _Options(int(lanes_per_element), int(range_mode), int(block_threads), int(kernel))
 
 
 def _call(prec, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element,
-          range_mode, block_threads):
+          range_mode, block_threads, kernel):
     import torch
     dtype = torch.float64 if prec == 64 else torch.float32
     n = v.numel()
@@ -131,7 +133,7 @@ def _call(prec, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element
     po = [_dev_ptr(t, dtype, n, nm) for t, nm in
           ((logk, "logk"), (dlogk_dv, "dlogk_dv"), (dlogk_dx, "dlogk_dx"))]
     L = lib()
-    o = _opts(lanes_per_element, range_mode, block_threads)
+    o = _opts(lanes_per_element, range_mode, block_threads, kernel)
     s = _stream_handle(stream)
     if o is None:
         f = L.bessel_logk_f64 if prec == 64 else L.bessel_logk_f32
@@ -143,18 +145,18 @@ def _call(prec, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element
 
 def bessel_logk_f64(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
                     stream=None, lanes_per_element=0, range_mode=BLK_RANGE_AUTO,
-                    block_threads=0):
+                    block_threads=0, kernel=BLK_KERNEL_AUTO):
     """Enqueue the FP64 kernel on ``stream`` writing into the given float64 CUDA tensors."""
     _call(64, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element,
-          range_mode, block_threads)
+          range_mode, block_threads, kernel)
 
 
 def bessel_logk_f32(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
                     stream=None, lanes_per_element=0, range_mode=BLK_RANGE_AUTO,
-                    block_threads=0):
+                    block_threads=0, kernel=BLK_KERNEL_AUTO):
     """Enqueue the FP32 kernel on ``stream`` writing into the given float32 CUDA tensors."""
     _call(32, v, x, logk, dlogk_dv, dlogk_dx, nbins, stream, lanes_per_element,
-          range_mode, block_threads)
+          range_mode, block_threads, kernel)
 
 
 def log_bessel_k(v, x, nbins=DEFAULT_NBINS, outputs=("logk", "dv", "dx"), **kw):

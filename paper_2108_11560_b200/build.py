@@ -47,16 +47,19 @@ def is_stale() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not is_stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines=()) -> str:
+    """Build the library (``out``/``defines`` only for tuning variants)."""
+    target = out or LIB
+    if out is None and not force and not is_stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC] + NVCC_FLAGS + ["-o", tmp] + sources()
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = [NVCC] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", tmp] + sources()
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -18,6 +18,8 @@
 #include "../../include/bessel_logk.h"
 #include "logk_quad.cuh"
 #include "logk_range.cuh"
+#include "logk_ws.cuh"
+#include "logk_split.cuh"
 
 namespace blk {
 
@@ -39,13 +41,14 @@ __device__ __forceinline__ void lane_bins(int n, int sub, int &mb, int &me) {
 }
 
 template <bool LOGK, bool DV, bool DX, int LPE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, BLK_MINB)
 logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 double *__restrict__ logk, double *__restrict__ dlogk_dv,
                 double *__restrict__ dlogk_dx, int nbins, int range_mode) {
-  __shared__ double tab[kExpTab];
-  fill_exp_table(tab);
+  __shared__ double tab_s[kTabSize];
+  load_exp_table(tab_s);
   __syncthreads();
+  const double *tab = lane_table(tab_s);
 
   const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t i = gtid / LPE;
@@ -58,25 +61,29 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   const double v = fabs(vraw);
   const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
 
-  double t0 = 0.0, t1 = 0.0, gp = 0.0;
+  // a2-a5: integration plan (t_p, g(t_p), t0, t1)
+  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      float tp32, gp32, t032, t132;
-      ok = make_plan<MathF32>(v, x, kLogEpsF64, tp32, gp32, t032, t132);
-      t0 = t032; t1 = t132; gp = gp32;
+      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64);
+      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
-      double tp64;
-      ok = make_plan<MathF64>(v, x, kLogEpsF64, tp64, gp, t0, t1);
+      const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
+      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
+  // a6: fixed-bin quadrature, three sums in one pass
   Sums64 s{0.0, 0.0, 0.0};
   const double h = (t1 - t0) / nbins;
   if (ok) {
     int mb, me;
     lane_bins<LPE>(nbins, sub, mb, me);
-    s = quad_f64<DV, DX>(v, x, t0, h, gp, nbins, mb, me, tab);
+    // exponent arguments stay above -707 unless the range reaches far below
+    // the eps level (never on valid ranges; kept exact for safety)
+    if (dmin > -600.0) s = quad_f64<DV, DX, false>(v, x, t0, h, gp, nbins, mb, me, tab);
+    else s = quad_f64<DV, DX, true>(v, x, t0, h, gp, nbins, mb, me, tab);
   }
   if (LPE > 1) {
     s.S0 = group_sum<LPE>(s.S0);
@@ -84,10 +91,12 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
     if (DX) s.S2 = group_sum<LPE>(s.S2);
   }
   if (!live || sub != 0) return;
+  // a7: epilogue
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
-  if (LOGK) logk[i] = ok ? gp + log(h) + log(s.S0) : nanv;
-  if (DV) dlogk_dv[i] = ok ? sgn * (s.S1 / s.S0) : nanv;
-  if (DX) dlogk_dx[i] = ok ? -(s.S2 / s.S0) : nanv;
+  const double r = rcp64(s.S0);
+  if (LOGK) logk[i] = ok ? gp + log(h * s.S0) : nanv;
+  if (DV) dlogk_dv[i] = ok ? sgn * (s.S1 * r) : nanv;
+  if (DX) dlogk_dx[i] = ok ? -(s.S2 * r) : nanv;
 }
 
 template <bool LOGK, bool DV, bool DX, int LPE>
@@ -109,12 +118,11 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      float tp;
-      ok = make_plan<MathF32>(v, x, kLogEpsF32, tp, gp, t0, t1);
+      const Plan<float> p = make_plan_f32(v, x, kLogEpsF32);
+      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp;
     } else {
-      double tp64, gp64, t064, t164;
-      ok = make_plan<MathF64>(v, x, kLogEpsF32, tp64, gp64, t064, t164);
-      t0 = (float)t064; t1 = (float)t164; gp = (float)gp64;
+      const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);
+      ok = p.ok; t0 = (float)p.t0; t1 = (float)p.t1; gp = (float)p.gp;
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
@@ -222,13 +230,17 @@ int auto_lanes(size_t n, int nbins) {
 template <class T>
 blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void *o2,
                     const void *o3, int nbins, const blk_options *opts, int &lanes,
-                    int &mode, int &threads) {
-  lanes = 0; mode = BLK_RANGE_AUTO; threads = blk::kDefaultThreads;
+                    int &mode, int &threads, int &kernel) {
+  lanes = 0; mode = BLK_RANGE_AUTO; threads = blk::kDefaultThreads; kernel = BLK_KERNEL_AUTO;
   if (opts) {
     lanes = opts->lanes_per_element;
     mode = opts->range_mode;
+    kernel = opts->kernel;
     if (opts->block_threads) threads = opts->block_threads;
   }
+  if (kernel < BLK_KERNEL_AUTO || kernel > BLK_KERNEL_WS) return fail(BLK_EINVAL, "bad kernel variant");
+  if (kernel == BLK_KERNEL_WS && lanes > 1) return fail(BLK_EINVAL, "the warp-specialized kernel has one element per lane");
+  if (kernel == BLK_KERNEL_WS && sizeof(T) != 8) return fail(BLK_EINVAL, "the warp-specialized kernel is FP64 only");
   if (nbins < 2 || nbins > BLK_MAX_NBINS) return fail(BLK_EINVAL, "nbins out of range [2, 65536]");
   if (n > 0 && !o1 && !o2 && !o3) return fail(BLK_EINVAL, "all outputs are NULL");
   if (n > 0 && (!v || !x)) return fail(BLK_EINVAL, "v or x is NULL");
@@ -236,7 +248,11 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
   if (lanes < 0 || lanes > 32 || (lanes & (lanes - 1))) return fail(BLK_EINVAL, "lanes_per_element must be 0 or a power of two <= 32");
   if (threads < 32 || threads > 128 || threads % 32) return fail(BLK_EINVAL, "block_threads must be a multiple of 32 in [32, 128]");
   if (n > ((size_t)1 << 40)) return fail(BLK_EINVAL, "n too large");
-  if (lanes == 0) lanes = auto_lanes(n, nbins);
+  // The warp-specialized kernel is measured slower on B200 (the path is
+  // issue-bound, so splitting the phases across warps adds nothing; see
+  // DESIGN.md §6): AUTO selects the simple kernel.
+  if (kernel == BLK_KERNEL_AUTO) kernel = BLK_KERNEL_SIMPLE;
+  if (lanes == 0) lanes = (kernel == BLK_KERNEL_WS) ? 1 : auto_lanes(n, nbins);
   return BLK_OK;
 }
 
@@ -262,15 +278,50 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
     default: return launch_k(KER<O1, O2, O3, 32>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
   }
 
+template <class K>
+blk_status launch_ws(K kern, size_t n, cudaStream_t st, const double *v, const double *x,
+                     double *a, double *b, double *c, int nbins, int mode) {
+  const size_t smem = sizeof(blk::WsShared);
+  int dev, sms = 0, per_sm = 0;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, blk::kWsThreads, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "ws occupancy query");
+  if (per_sm < 1) return fail(BLK_ECUDA, "ws kernel cannot be resident");
+  const size_t tiles = (n + 31) / 32;
+  size_t grid = (size_t)sms * per_sm;
+  if (grid > tiles) grid = tiles;
+  kern<<<(unsigned)grid, blk::kWsThreads, smem, st>>>(v, x, n, a, b, c, nbins, mode);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "ws kernel launch");
+  return BLK_OK;
+}
+
+#define BLK_WS(O1, O2, O3) \
+  return launch_ws(blk::logk_f64_ws_kernel<O1, O2, O3>, n, stream, v, x, a, b, c, nbins, mode);
+
 template <class T>
 blk_status run(const T *v, const T *x, size_t n, T *a, T *b, T *c, int nbins,
                const blk_options *opts, cudaStream_t stream) {
-  int lanes, mode, th;
-  blk_status st = validate(v, x, n, a, b, c, nbins, opts, lanes, mode, th);
+  int lanes, mode, th, kernel;
+  blk_status st = validate(v, x, n, a, b, c, nbins, opts, lanes, mode, th, kernel);
   if (st != BLK_OK) return st;
   if (n == 0) return BLK_OK;
   const int sel = (a ? 4 : 0) | (b ? 2 : 0) | (c ? 1 : 0);
   if constexpr (sizeof(T) == 8) {
+    if (kernel == BLK_KERNEL_WS) {
+      switch (sel) {
+        case 7: BLK_WS(true, true, true)
+        case 6: BLK_WS(true, true, false)
+        case 5: BLK_WS(true, false, true)
+        case 4: BLK_WS(true, false, false)
+        case 3: BLK_WS(false, true, true)
+        case 2: BLK_WS(false, true, false)
+        default: BLK_WS(false, false, true)
+      }
+    }
     switch (sel) {
       case 7: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, true, true)
       case 6: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, true, false)
@@ -359,8 +410,8 @@ size_t bessel_logk_host_workspace_bytes(size_t chunk, size_t elem_bytes) {
 blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, double *logk,
                                 double *dlogk_dv, double *dlogk_dx, int nbins, void *workspace,
                                 size_t workspace_bytes, size_t chunk, cudaStream_t stream) {
-  int lanes, mode, th;
-  blk_status st = validate(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, nullptr, lanes, mode, th);
+  int lanes, mode, th, kernel;
+  blk_status st = validate(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, nullptr, lanes, mode, th, kernel);
   if (st != BLK_OK) return st;
   if (n == 0) return BLK_OK;
   if (chunk == 0) chunk = (size_t)1 << 20;
@@ -391,7 +442,9 @@ blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, doub
       return cuda_fail(e, "H2D v");
     if ((e = cudaMemcpyAsync(dx_, x + off, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       return cuda_fail(e, "H2D x");
-    blk_options o{lanes, mode, th};
+    // one element per lane in every chunk: results do not depend on the
+    // chunking and equal a device-path call with lanes_per_element = 1
+    blk_options o{1, mode, th, BLK_KERNEL_SIMPLE};
     st = run<double>(dv_, dx_, m, logk ? o0 : nullptr, dlogk_dv ? o1 : nullptr,
                      dlogk_dx ? o2 : nullptr, nbins, &o, s);
     if (st != BLK_OK) return st;
@@ -409,6 +462,22 @@ blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, doub
   cudaEventDestroy(start_ev);
   if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "synchronize");
   return BLK_OK;
+}
+
+blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, double *logk,
+                               double *dlogk_dv, double *dlogk_dx, int nbins, void *scratch,
+                               int phases, cudaStream_t s) {
+  if (!v || !x || !logk || !dlogk_dv || !dlogk_dx || !scratch || nbins < 2 || nbins > BLK_MAX_NBINS)
+    return fail(BLK_EINVAL, "bad split args");
+  if (n == 0) return BLK_OK;
+  const unsigned blocks = (unsigned)((n + 127) / 128);
+  blk::PlanRec *plans = (blk::PlanRec *)scratch;
+  if (phases & 1) blk::plan_f64_kernel<<<blocks, 128, 0, s>>>(v, x, n, plans, nbins, 0);
+  if (phases & 2)
+    blk::quad_f64_kernel<true, true, true><<<blocks, 128, 0, s>>>(v, x, n, plans, logk, dlogk_dv,
+                                                                  dlogk_dx, nbins);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "split kernels");
 }
 
 blk_status blk_microbench_fp64(int blocks, int threads, int iters, double *out, cudaStream_t s) {

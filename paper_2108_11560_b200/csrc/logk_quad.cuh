@@ -7,9 +7,11 @@
 //   t tanh(vt) exp(g(t) - s)      = E t (1 - q)
 //   cosh t exp(g(t) - s)          = E (1 + q) cosh t
 // so one exponential per node carries all three sums.  e^{+-t} and q advance
-// by geometric recurrences (re-anchored every kAnchor nodes for e^{+-t});
+// by geometric recurrences (e^{+-t} re-anchored every kAnchor nodes);
 // p = 1 - q advances additively, p' = p + q (1 - e^{-2vh}), which has no
-// cancellation for small vt (R21).
+// cancellation for small vt (R21).  The half weights of the two
+// end nodes are applied after the loop so the loop body carries
+// no per-node select.
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
@@ -20,89 +22,273 @@
 namespace blk {
 
 constexpr int kExpTab = 256;      // 2^(j/256), j = 0..255, in shared memory
-constexpr int kAnchor = 32;       // FP64 re-anchoring interval for e^{+-t}
+#ifndef BLK_TAB_REP
+#define BLK_TAB_REP 1
+#endif
+// The table can be stored kTabRep times, interleaved (entry j of copy c at
+// j*kTabRep + c), with lane L reading copy L % kTabRep: 16 copies make the
+// per-node LDS.64 bank-conflict-free.  Measured on B200 (profiles/r01_*):
+// no gain -- the kernel is issue-bound, not LDS-bound -- and the 32 KB table
+// fill costs more, so the default is a single copy.
+constexpr int kTabRep = BLK_TAB_REP;
+constexpr int kTabSize = kExpTab * kTabRep;
+constexpr int kAnchor = 36;       // FP64 re-anchoring interval for e^{+-t} (max)
+#ifndef BLK_GROUP
+#define BLK_GROUP 4
+#endif
+#ifndef BLK_ACC2
+#define BLK_ACC2 0
+#endif
+#ifndef BLK_MINB
+#define BLK_MINB 6
+#endif
+constexpr int kGroup = BLK_GROUP; // nodes evaluated together (independent exp chains)
+constexpr bool kAcc2 = BLK_ACC2;  // split the sums over two accumulator sets
+#ifndef BLK_LOCKSTEP
+#define BLK_LOCKSTEP 1
+#endif
+constexpr bool kLockstep = BLK_LOCKSTEP;  // stage-by-stage evaluation of a group
 
-// exp(a) for a in [-707, 709] by Tang's table method: a = (k/256) ln2 + r,
-// |r| <= ln2/512, exp(a) = 2^(k>>8) * T[k&255] * (1 + r + r^2/2 + r^3/6 + r^4/24).
-// Inputs below -707 are clamped (the weight is < 1e-307 of the peak there).
-// ~10 FP64-pipe instructions + 1 LDS.64 + 3 integer ops.
+__device__ const double kExp2Table[kExpTab] = {
+#include "exp2_table.inc"
+};
+
+// Block-cooperative copy of the table to shared memory (caller syncs).
+// tab has kTabSize doubles.
+__device__ __forceinline__ void load_exp_table(double *tab) {
+  for (int j = threadIdx.x; j < kTabSize; j += blockDim.x) tab[j] = kExp2Table[j / kTabRep];
+}
+// This lane's copy of the table (pass the result to exp_tab).
+__device__ __forceinline__ const double *lane_table(const double *tab) {
+  return tab + (threadIdx.x % kTabRep);
+}
+
+// exp(a) by Tang's table method: a = (k/256) ln2 + r, |r| <= ln2/512,
+// exp(a) = 2^(k>>8) * T[k&255] * (1 + r + r^2/2 + r^3/6 + r^4/24).
+// Valid for a in [-707, 709]; CLAMP maps a < -707 to e^-707 (caller decides
+// whether its arguments can leave the range -- see quad_f64).
+// 8 FP64-pipe instructions + 1 LDS.64 + 5 integer ops.
+constexpr double kExpInvL = 369.3299304675746;       // 256 / ln 2
+constexpr double kExpMagic = 6755399441055744.0;     // 1.5 * 2^52: round-to-int trick
+constexpr double kExpC = 0.0027076061740622863;      // ln2/256 (single-step reduction:
+                                                     // |k| <= 2^18 -> |error| < 1.2e-13 |a|/707)
+template <bool CLAMP>
 __device__ __forceinline__ double exp_tab(double a, const double *__restrict__ tab) {
-  const double kInvL = 369.3299304675746;             // 256 / ln 2
-  const double kMagic = 6755399441055744.0;            // 1.5 * 2^52: round-to-int trick
-  const double kC1 = 0.00270760617331689;              // ln2/256 to 32 bits: k*kC1 exact
-  const double kC2 = 7.453964567463233e-13;            // ln2/256 - kC1
-  a = fmax(a, -707.0);
-  double kd = fma(a, kInvL, kMagic);
+  if (CLAMP) a = a < -707.0 ? -707.0 : a;
+  double kd = fma(a, kExpInvL, kExpMagic);
   const int k = __double2loint(kd);
-  kd -= kMagic;
-  double r = fma(kd, -kC1, a);                         // Cody-Waite reduction
-  r = fma(kd, -kC2, r);
+  kd -= kExpMagic;
+  const double r = fma(kd, -kExpC, a);
   double p = fma(r, 4.1666666666666666e-02, 1.6666666666666666e-01);
   p = fma(p, r, 0.5);
-  p = fma(p, r * r, r);
-  double tj = tab[k & (kExpTab - 1)];
-  double res = fma(tj, p, tj);
-  int hi = __double2hiint(res) + ((k >> 8) << 20);
+  p = fma(p, r * r, r);                               // e^r - 1
+  const double tj = tab[(k & (kExpTab - 1)) * kTabRep];
+  const double res = fma(tj, p, tj);
+  const int hi = __double2hiint(res) + ((k >> 8) << 20);
   return __hiloint2double(hi, __double2loint(res));
 }
 
-// Same as exp_tab but safe for any finite a (anchors: t itself may be large).
-__device__ __forceinline__ double exp_anchor(double a, const double *__restrict__ tab) {
-  return a > 709.0 ? (double)INFINITY : exp_tab(a, tab);
+// 1/a to ~1 ulp: MUFU.RCP64H seed + two Newton steps.
+__device__ __forceinline__ double rcp64(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
 }
 
-// Fill the 2^(j/256) table (block-cooperative; caller syncs).
-__device__ __forceinline__ void fill_exp_table(double *tab) {
-  for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
+// 1 - e^z for z <= 0 without cancellation (-expm1(z)).
+__device__ __forceinline__ double one_minus_exp(double z, const double *__restrict__ tab) {
+  if (z < -0.34657359027997264) return 1.0 - exp_tab<true>(z, tab);
+  // Taylor series of -(e^z - 1) to z^14 (|z| <= ln2/2: truncation < 3e-18 |z|)
+  double p = 1.0 / 87178291200.0;   // 1/14!
+  p = fma(p, z, 1.0 / 6227020800.0);
+  p = fma(p, z, 1.0 / 479001600.0);
+  p = fma(p, z, 1.0 / 39916800.0);
+  p = fma(p, z, 1.0 / 3628800.0);
+  p = fma(p, z, 1.0 / 362880.0);
+  p = fma(p, z, 1.0 / 40320.0);
+  p = fma(p, z, 1.0 / 5040.0);
+  p = fma(p, z, 1.0 / 720.0);
+  p = fma(p, z, 1.0 / 120.0);
+  p = fma(p, z, 1.0 / 24.0);
+  p = fma(p, z, 1.0 / 6.0);
+  p = fma(p, z, 0.5);
+  p = fma(p, z, 1.0);
+  return -(p * z);
 }
 
 struct Sums64 {
   double S0, S1, S2;
 };
 
-// Nodes m in [mb, me) of the n-interval trapezoid on [t0, t0 + n h]; node 0
-// and node n carry weight 1/2 via a log-2 larger shift.
+// One node's contributions, given cosh t, q = e^{-2vt} and p = 1 - q.
+template <bool DV, bool DX, bool CLAMP>
+__device__ __forceinline__ void node_acc(double v, double x, double s_mid, double t, double ch,
+                                         double q, double p, const double *__restrict__ tab,
+                                         double &S0, double &S1, double &S2) {
+  const double E = exp_tab<CLAMP>(fma(-x, ch, fma(v, t, -s_mid)), tab);
+  const double w = fma(E, q, E);                     // E (1 + q)
+  S0 += w;
+  if (DX) S2 = fma(w, ch, S2);
+  if (DV) S1 = fma(E * t, p, S1);
+}
+
+// Nodes [ib, ie) with weight 1.  Node positions are t0 + m h to 1 ulp (an
+// accumulated t += h would drift by m ulp, which v t amplifies for large v);
+// e^{+-t} are re-anchored every kAnchor nodes, q and p advance across chunks.
+template <bool DV, bool DX, bool CLAMP>
+__device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double h,
+                                           double s_mid, int ib, int ie,
+                                           const double *__restrict__ tab, Sums64 &s) {
+  if (ie <= ib) return;
+  const double m2v = -2.0 * v;
+  const double eh = exp_tab<false>(h, tab);
+  const double ehi = rcp64(eh);
+  const double tb = fma((double)ib, h, t0);
+  double q = exp_tab<true>(m2v * tb, tab);           // q_m = e^{-2 v t_m}
+  const double eq = exp_tab<true>(m2v * h, tab);
+  double p = DV ? one_minus_exp(m2v * tb, tab) : 0.0;  // p_m = 1 - q_m
+  const double a1 = DV ? one_minus_exp(m2v * h, tab) : 0.0;
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+  double T0 = 0.0, T1 = 0.0, T2 = 0.0;               // second accumulator set (kAcc2)
+  // chunks of <= kAnchor nodes, equal sizes rounded up to whole groups
+  const int nch = (ie - ib + kAnchor - 1) / kAnchor;
+  const int csz = ((ie - ib + nch - 1) / nch + kGroup - 1) / kGroup * kGroup;
+#pragma unroll 1
+  for (int c0 = ib; c0 < ie; c0 += csz) {
+    const int c1 = min(c0 + csz, ie);
+    double tc = fma((double)c0, h, t0);
+    double et = 0.5 * exp_tab<true>(fmin(tc, 709.0), tab);   // e^t / 2
+    double eti = 0.25 * rcp64(et);                           // e^-t / 2
+    if (c0 == 0) {
+      // node 0 has weight 1/2: take half of it back.  It is exact
+      // here (anchored state) and may be the largest node (t0 = 0 when the
+      // peak region reaches t = 0), so this correction is done in FP64.
+      double h0 = 0.0, h1 = 0.0, h2 = 0.0;
+      node_acc<DV, DX, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, h0, h1, h2);
+      S0 -= 0.5 * h0; S1 -= 0.5 * h1; S2 -= 0.5 * h2;
+    }
+    int m = c0;
+#pragma unroll 1
+    for (; m + kGroup <= c1; m += kGroup) {          // groups of kGroup nodes
+      double tg[kGroup], chg[kGroup], qg[kGroup], pg[kGroup];
+#pragma unroll
+      for (int j = 0; j < kGroup; ++j) {
+        tg[j] = j == 0 ? tc : fma(double(j), h, tc);
+        chg[j] = et + eti;
+        et *= eh;
+        eti *= ehi;
+        qg[j] = q;
+        pg[j] = p;
+        if (DV) p = fma(q, a1, p);
+        q *= eq;
+      }
+      if (kLockstep) {
+        // the group's exponentials stage by stage, so consecutive dependent
+        // FP64 instructions of one node are kGroup instructions apart
+        double a[kGroup], kd[kGroup], r[kGroup], pp[kGroup], E[kGroup];
+        int k[kGroup];
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) a[j] = fma(v, tg[j], -s_mid);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          a[j] = fma(-x, chg[j], a[j]);
+          if (CLAMP) a[j] = a[j] < -707.0 ? -707.0 : a[j];
+        }
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) kd[j] = fma(a[j], kExpInvL, kExpMagic);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) { k[j] = __double2loint(kd[j]); kd[j] -= kExpMagic; }
+        double tj[kGroup];
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) tj[j] = tab[(k[j] & (kExpTab - 1)) * kTabRep];
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) pp[j] = fma(r[j], 4.1666666666666666e-02, 1.6666666666666666e-01);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j], 0.5);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j] * r[j], r[j]);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          const double res = fma(tj[j], pp[j], tj[j]);
+          E[j] = __hiloint2double(__double2hiint(res) + ((k[j] >> 8) << 20), __double2loint(res));
+        }
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          const double w = fma(E[j], qg[j], E[j]);
+          if (kAcc2 && (j & 1)) {
+            T0 += w;
+            if (DX) T2 = fma(w, chg[j], T2);
+            if (DV) T1 = fma(E[j] * tg[j], pg[j], T1);
+          } else {
+            S0 += w;
+            if (DX) S2 = fma(w, chg[j], S2);
+            if (DV) S1 = fma(E[j] * tg[j], pg[j], S1);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          if (kAcc2 && (j & 1))
+            node_acc<DV, DX, CLAMP>(v, x, s_mid, tg[j], chg[j], qg[j], pg[j], tab, T0, T1, T2);
+          else
+            node_acc<DV, DX, CLAMP>(v, x, s_mid, tg[j], chg[j], qg[j], pg[j], tab, S0, S1, S2);
+        }
+      }
+      tc = fma((double)(m + kGroup), h, t0);
+    }
+#pragma unroll 1
+    for (; m < c1; ++m) {                            // remainder
+      node_acc<DV, DX, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, S0, S1, S2);
+      if (DV) p = fma(q, a1, p);
+      q *= eq;
+      et *= eh; eti *= ehi;
+      tc = fma((double)(m + 1), h, t0);
+    }
+  }
+  s.S0 += S0 + T0;
+  s.S1 += S1 + T1;
+  s.S2 += S2 + T2;
+}
+
+// Half of the last node's contributions, evaluated in FP32: that node sits
+// below the eps level of the peak (d(t1) < 0), so its terms are < 2^-52 of
+// the sums and FP32 is exact to far below double rounding there.
 template <bool DV, bool DX>
+__device__ __forceinline__ void end_half_f32(double v, double x, double s_mid, double t,
+                                             Sums64 &s) {
+  const float kL2e = 1.4426950408889634f;
+  const float tf = float(t), vf = float(v);
+  const float e = ex2_approx(tf * kL2e);
+  const float ch = 0.5f * (e + rcp_approx(e));
+  const float q = ex2_approx(-2.0f * vf * kL2e * tf);
+  const float arg = float(fma(v, t, -s_mid) - x * double(ch));
+  const float E = 0.5f * ex2_approx(arg * kL2e);
+  const float w = fmaf(E, q, E);
+  if (!(w > 0.0f)) return;          // underflowed (or e^t overflowed FP32): nothing to take back
+  s.S0 -= w;
+  if (DX) s.S2 -= double(w) * ch;
+  if (DV) s.S1 -= double(E * tf) * (-expm1f(-2.0f * vf * tf));
+}
+
+// Nodes [mb, me) of the n-interval trapezoid on [t0, t0 + n h] (node m at
+// t0 + m h; nodes 0 and n carry weight 1/2: all nodes are summed
+// with weight 1 and half of each end node is taken back).  The lane owning
+// node 0 has mb == 0, the lane owning node n has me == n + 1.
+template <bool DV, bool DX, bool CLAMP>
 __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double h,
                                            double shift, int n, int mb, int me,
                                            const double *__restrict__ tab) {
   Sums64 s{0.0, 0.0, 0.0};
-  const double s_mid = shift + kLn2;          // E = exp(vt - x cosh t - s_mid)
-  const double s_end = s_mid + kLn2;          // half weight
-  const double eh = exp(h), ehi = exp(-h);
-  const double m2v = -2.0 * v;
-  double tb = fma((double)mb, h, t0);
-  double q = exp(m2v * tb);                   // q_m = e^{-2 v t_m}
-  const double eq = exp(m2v * h);
-  double p = -expm1(m2v * tb);                // p_m = 1 - q_m without cancellation
-  const double a1 = -expm1(m2v * h);
-  const int cnt = me - mb;
-  if (cnt <= 0) return s;
-  const int nch = (cnt + kAnchor - 1) / kAnchor;
-  const int csz = (cnt + nch - 1) / nch;
-#pragma unroll 1
-  for (int c0 = mb; c0 < me; c0 += csz) {
-    const int c1 = min(c0 + csz, me);
-    double t = fma((double)c0, h, t0);
-    double et = 0.5 * exp_anchor(t, tab);     // e^t / 2
-    double eti = 0.5 * exp_tab(-t, tab);      // e^-t / 2
-#pragma unroll 4
-    for (int m = c0; m < c1; ++m) {
-      const double ch = et + eti;             // cosh t
-      const double sm = (m == 0 || m == n) ? s_end : s_mid;
-      const double arg = fma(-x, ch, fma(v, t, -sm));
-      const double E = exp_tab(arg, tab);
-      const double w = fma(E, q, E);          // E (1 + q)
-      s.S0 += w;
-      if (DX) s.S2 = fma(w, ch, s.S2);
-      if (DV) s.S1 = fma(E * t, p, s.S1);
-      if (DV) p = fma(q, a1, p);
-      q *= eq;
-      t += h;
-      et *= eh;
-      eti *= ehi;
-    }
-  }
+  const double s_mid = shift + kLn2;                 // E = exp(vt - x cosh t - s_mid)
+  nodes_fp64<DV, DX, CLAMP>(v, x, t0, h, s_mid, mb, me, tab, s);
+  // node n: t_n = t1 lies outside the eps-support (d(t1) < 0, FindZero
+  // returns the outer end, R1), so its term is < 2^-52 of the peak term
+  if (me == n + 1) end_half_f32<DV, DX>(v, x, s_mid, fma((double)n, h, t0), s);
   return s;
 }
 

@@ -6,14 +6,18 @@
 // R4 fixed 10 iterations; R5 lo = t_s when m = 0; R18 Newton with F'(a)=0
 // -> bisection point).  Independent of oracle/ (no shared code).
 //
-// Templated on the working type T and a math policy:
-//   MathF32: FP32 FMA pipe + MUFU (ex2/lg2/rcp.approx).  The plan only needs
-//            to be conservative at the log-eps level (R20), so the
-//            range is found here and the quadrature (FP64 pipe) consumes it.
-//   MathF64: libdevice double functions -- the paper's working-precision
-//            variant, used outside the FP32-safe domain and on request.
+// Two implementations of the same algorithm:
+//   * PlanF32: FP32 FMA pipe + MUFU (ex2/lg2/rcp.approx).  The two point
+//     evaluations of one FindZero iteration (at the bisection point and at the
+//     Newton point) are independent, so they run as packed f32x2 operations
+//     (FFMA2/FADD2/FMUL2, sm_100) -- half the issue slots.  The plan only has
+//     to be conservative at the log-eps level (R20), so finding it
+//     in FP32 leaves the FP64 pipe to the quadrature.
+//   * PlanF64: libdevice double functions -- the paper's working-precision
+//     variant; used outside the FP32-safe domain and on request
+//     (BLK_RANGE_F64).
 // Every point evaluation returns F and F' jointly (they share e^t, e^-t and
-// q = e^{-2vt}), so one FindZero iteration costs two joint evaluations.
+// q = e^{-2vt}).
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
@@ -42,72 +46,123 @@ __device__ __forceinline__ float rcp_approx(float a) {
   return y;
 }
 
-struct MathF32 {
-  using T = float;
-  static constexpr float kLog2e = 1.4426950408889634f;
+// ------------------------------------------------------------ packed helpers
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 ex2_2(float2 a) { return f2(ex2_approx(a.x), ex2_approx(a.y)); }
+__device__ __forceinline__ float2 lg2_2(float2 a) { return f2(lg2_approx(a.x), lg2_approx(a.y)); }
+__device__ __forceinline__ float2 rcp_2(float2 a) { return f2(rcp_approx(a.x), rcp_approx(a.y)); }
+
+// Result of the range finding for one element.
+template <class T>
+struct Plan {
+  T tp, gp, t0, t1;
+  T dmin;     // min of d = g - g(t_p) - log eps at t0 and t1 (for the exp-clamp decision)
+  bool ok;
+};
+
+// ============================================================== FP32 (packed)
+struct PlanF32 {
+  static constexpr float kL2e = 1.4426950408889634f;
   static constexpr float kLn2f = 0.6931471805599453f;
-  // exp(a) for an argument pre-multiplied by log2(e)
-  __device__ __forceinline__ static float exp2s(float a2) { return ex2_approx(a2); }
-  __device__ __forceinline__ static float scale(float a) { return a * kLog2e; }
-  // log(1 + q), q in [0, 1]
-  __device__ __forceinline__ static float log1p01(float q) { return lg2_approx(1.0f + q) * kLn2f; }
-  __device__ __forceinline__ static float rcp(float a) { return rcp_approx(a); }
-  __device__ __forceinline__ static float div(float a, float b) { return __fdividef(a, b); }
-};
+  float v, x, hx, v2, m2vs, L;
 
-struct MathF64 {
-  using T = double;
-  __device__ __forceinline__ static double exp2s(double a) { return exp(a); }
-  __device__ __forceinline__ static double scale(double a) { return a; }
-  __device__ __forceinline__ static double log1p01(double q) { return log1p(q); }
-  __device__ __forceinline__ static double rcp(double a) { return 1.0 / a; }
-  __device__ __forceinline__ static double div(double a, double b) { return a / b; }
-};
-
-// F = g'(t) = v tanh(vt) - x sinh t,  F' = g''(t) = v^2 sech^2(vt) - x cosh t
-// (Eq. 4-5).  tanh = (1-q)/(1+q), sech^2 = 4q/(1+q)^2, q = e^{-2vt}.
-template <class M>
-struct PeakFn {
-  using T = typename M::T;
-  T v, hx, v2, m2vs, ones;  // hx = x/2, v2 = v^2, m2vs = scale(-2v), ones = scale(1)
-  __device__ __forceinline__ void operator()(T t, T &F, T &dF) const {
-    T e = M::exp2s(ones * t);
-    T ei = M::rcp(e);
-    T q = M::exp2s(m2vs * t);
-    T r = M::rcp(T(1) + q);
-    T th = (T(1) - q) * r;
-    T s2 = T(4) * q * r * r;
-    F = v * th - hx * (e - ei);
-    dF = v2 * s2 - hx * (e + ei);
+  // F = g'(t) = v tanh(vt) - x sinh t,  F' = g''(t) = v^2 sech^2(vt) - x cosh t
+  // (Eq. 4-5);  tanh = (1-q)/(1+q), sech^2 = 4q/(1+q)^2, q = e^{-2vt}.
+  __device__ __forceinline__ void peak1(float t, float &F, float &dF) const {
+    float e = ex2_approx(t * kL2e), ei = rcp_approx(e);
+    float q = ex2_approx(m2vs * t), r = rcp_approx(1.0f + q);
+    F = v * ((1.0f - q) * r) - hx * (e - ei);
+    dF = v2 * (4.0f * q * r * r) - hx * (e + ei);
+  }
+  __device__ __forceinline__ void peak2(float2 t, float2 &F, float2 &dF) const {
+    float2 e = ex2_2(mul2(t, f2s(kL2e)));
+    float2 ei = rcp_2(e);
+    float2 q = ex2_2(mul2(t, f2s(m2vs)));
+    float2 r = rcp_2(add2(q, f2s(1.0f)));
+    float2 th = mul2(add2(f2s(1.0f), mul2(q, f2s(-1.0f))), r);
+    float2 s2 = mul2(mul2(q, f2s(4.0f)), mul2(r, r));
+    F = fma2(f2s(v), th, mul2(f2s(-hx), add2(e, mul2(ei, f2s(-1.0f)))));
+    dF = fma2(f2s(v2), s2, mul2(f2s(-hx), add2(e, ei)));
+  }
+  // F = d(t) = g(t) - g(t_p) - log eps, F' = g'(t);
+  // g(t) = vt + log(1+q) - log 2 - x cosh t, c = g(t_p) + log eps + log 2.
+  __device__ __forceinline__ void thr1(float c, float t, float &F, float &dF) const {
+    float e = ex2_approx(t * kL2e), ei = rcp_approx(e);
+    float q = ex2_approx(m2vs * t), r = rcp_approx(1.0f + q);
+    F = v * t + lg2_approx(1.0f + q) * kLn2f - hx * (e + ei) - c;
+    dF = v * ((1.0f - q) * r) - hx * (e - ei);
+  }
+  __device__ __forceinline__ void thr2(float c, float2 t, float2 &F, float2 &dF) const {
+    float2 e = ex2_2(mul2(t, f2s(kL2e)));
+    float2 ei = rcp_2(e);
+    float2 q = ex2_2(mul2(t, f2s(m2vs)));
+    float2 opq = add2(q, f2s(1.0f));
+    float2 r = rcp_2(opq);
+    float2 lq = lg2_2(opq);
+    float2 base = fma2(lq, f2s(kLn2f), f2s(-c));
+    base = fma2(f2s(v), t, base);
+    F = fma2(f2s(-hx), add2(e, ei), base);
+    float2 omq = add2(f2s(1.0f), mul2(q, f2s(-1.0f)));
+    dF = fma2(mul2(f2s(v), omq), r, mul2(f2s(-hx), add2(e, mul2(ei, f2s(-1.0f)))));
+  }
+  __device__ __forceinline__ float gval(float t) const {
+    float e = ex2_approx(t * kL2e), ei = rcp_approx(e);
+    float q = ex2_approx(m2vs * t);
+    return v * t + lg2_approx(1.0f + q) * kLn2f - float(kLn2) - hx * (e + ei);
   }
 };
 
-// F = d(t) = g(t) - g(t_p) - log eps,  F' = g'(t)
-// g(t) = vt + log(1+q) - log 2 - x cosh t;  c = g(t_p) + log eps + log 2.
-template <class M>
-struct ThreshFn {
-  using T = typename M::T;
-  T v, hx, m2vs, ones, c;
-  __device__ __forceinline__ void operator()(T t, T &F, T &dF) const {
-    T e = M::exp2s(ones * t);
-    T ei = M::rcp(e);
-    T q = M::exp2s(m2vs * t);
-    T r = M::rcp(T(1) + q);
-    F = v * t + M::log1p01(q) - hx * (e + ei) - c;
-    dF = v * (T(1) - q) * r - hx * (e - ei);
-  }
-};
+// One FindZero iteration, shared by both precisions: bisection
+// point mid, clipped Newton point tn (R2, R3, R18) ...
+template <class T>
+__device__ __forceinline__ void fz_points(T a, T Fa, T dFa, T b, T &mid, T &tn) {
+  mid = a + (b - a) * T(0.5);                    // t_shrink
+  T t = a - Fa / dFa;                            // t_newton from the current a (R2)
+  t = isfinite(t) ? t : mid;                     // F'(a) = 0 or overflow (R18)
+  T lo = fmin(a, mid), hi = fmax(a, mid);        // Clip to [a, mid] (R3)
+  tn = fmin(fmax(t, lo), hi);
+}
+__device__ __forceinline__ void fz_points_f32(float a, float Fa, float dFa, float b, float &mid,
+                                              float &tn) {
+  mid = a + (b - a) * 0.5f;
+  float t = a - Fa * rcp_approx(dFa);
+  t = isfinite(t) ? t : mid;
+  float lo = fminf(a, mid), hi = fmaxf(a, mid);
+  tn = fminf(fmaxf(t, lo), hi);
+}
 
-// g(t) itself (Eq. 3), for g(t_p).
-template <class M>
-__device__ __forceinline__ typename M::T g_value(typename M::T v, typename M::T hx,
-                                                 typename M::T m2vs, typename M::T ones,
-                                                 typename M::T t) {
-  using T = typename M::T;
-  T e = M::exp2s(ones * t);
-  T ei = M::rcp(e);
-  T q = M::exp2s(m2vs * t);
-  return v * t + M::log1p01(q) - T(kLn2) - hx * (e + ei);
+// ... then the three-way bracket update, branch-free.
+template <class T>
+__device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt, T &a, T &Fa,
+                                          T &dFa, T &b) {
+  const bool c1 = Fm < T(0);                     // zero in (mid, b)
+  const bool c2 = Ft < T(0);                     // zero in (tn, mid)
+  //                                                else zero in (a, tn)
+  const T na = c1 ? mid : (c2 ? tn : a);
+  const T nFa = c1 ? Fm : (c2 ? Ft : Fa);
+  const T ndFa = c1 ? dFm : (c2 ? dFt : dFa);
+  b = c1 ? b : (c2 ? mid : tn);
+  a = na; Fa = nFa; dFa = ndFa;
+}
+
+// Alg. 2 with the two evaluations packed into f32x2 operations.
+template <bool PEAK>
+__device__ __forceinline__ float find_zero_f32(const PlanF32 &P, float c, float a, float &Fa,
+                                               float dFa, float b) {
+#pragma unroll 1
+  for (int i = 0; i < kMaxIter; ++i) {
+    float mid, tn;
+    fz_points_f32(a, Fa, dFa, b, mid, tn);
+    float2 F, dF;
+    if (PEAK) P.peak2(f2(mid, tn), F, dF);
+    else P.thr2(c, f2(mid, tn), F, dF);
+    fz_update<float>(mid, tn, F.x, dF.x, F.y, dF.y, a, Fa, dFa, b);
+  }
+  return a;
 }
 
 // Alg. 1 FindRange from t_s with F(t_s) >= 0.  Returns false when
@@ -129,58 +184,92 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
   return true;
 }
 
-// Alg. 2 FindZero, fixed kMaxIter iterations, F(a) < 0 <= F(b).
-template <class M, class Fn, class T>
-__device__ __forceinline__ T find_zero(const Fn &f, T a, T Fa, T dFa, T b) {
+// Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
+// is taken in double on the caller's inputs.
+__device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps) {
+  Plan<float> p;
+  PlanF32 P;
+  P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
+  P.m2vs = -2.0f * P.v * PlanF32::kL2e; P.L = float(log_eps);
+  float lo, hi, Fh, dFh;
+  p.ok = false;
+  p.tp = 0.0f;
+  if (vd * vd - xd > 0.0) {
+    auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
+    if (!find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
+    p.tp = find_zero_f32<true>(P, 0.0f, hi, Fh, dFh, lo);         // (t_e, t_s)
+  }
+  p.gp = P.gval(p.tp);
+  const float c = p.gp + P.L + float(kLn2);
+  p.t0 = 0.0f;
+  float d0 = -P.x - p.gp - P.L;                                    // d(0)
+  if (d0 <= 0.0f) p.t0 = find_zero_f32<false>(P, c, 0.0f, d0, 0.0f, p.tp);
+  auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
+  if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
+  p.t1 = find_zero_f32<false>(P, c, hi, Fh, dFh, lo);
+  p.dmin = fminf(d0, Fh);
+  p.ok = true;
+  return p;
+}
+
+// ==================================================================== FP64
+struct PlanF64 {
+  double v, x, hx, v2, m2v;
+  __device__ __forceinline__ void peak(double t, double &F, double &dF) const {
+    double e = exp(t), ei = 1.0 / e;
+    double q = exp(m2v * t), r = 1.0 / (1.0 + q);
+    F = v * ((1.0 - q) * r) - hx * (e - ei);
+    dF = v2 * (4.0 * q * r * r) - hx * (e + ei);
+  }
+  __device__ __forceinline__ void thr(double c, double t, double &F, double &dF) const {
+    double e = exp(t), ei = 1.0 / e;
+    double q = exp(m2v * t), r = 1.0 / (1.0 + q);
+    F = v * t + log1p(q) - hx * (e + ei) - c;
+    dF = v * ((1.0 - q) * r) - hx * (e - ei);
+  }
+  __device__ __forceinline__ double gval(double t) const {
+    double e = exp(t), ei = 1.0 / e;
+    return v * t + log1p(exp(m2v * t)) - kLn2 - hx * (e + ei);
+  }
+};
+
+template <class Fn>
+__device__ __forceinline__ double find_zero_f64(const Fn &f, double a, double &Fa, double dFa,
+                                                double b) {
 #pragma unroll 1
   for (int i = 0; i < kMaxIter; ++i) {
-    T mid = a + (b - a) * T(0.5);                 // t_shrink
-    T tn = a - M::div(Fa, dFa);                   // t_newton from the current a (R2)
-    if (!isfinite(tn)) tn = mid;                  // F'(a) = 0 (R18)
-    T lo = fmin(a, mid), hi = fmax(a, mid);       // Clip to [a, mid] (R3)
-    tn = fmin(fmax(tn, lo), hi);
-    T Fm, dFm, Ft, dFt;
+    double mid, tn;
+    fz_points<double>(a, Fa, dFa, b, mid, tn);
+    double Fm, dFm, Ft, dFt;
     f(mid, Fm, dFm);
     f(tn, Ft, dFt);
-    if (Fm < T(0)) {
-      a = mid; Fa = Fm; dFa = dFm;
-    } else if (Ft < T(0)) {
-      b = mid; a = tn; Fa = Ft; dFa = dFt;
-    } else {
-      b = tn;
-    }
+    fz_update<double>(mid, tn, Fm, dFm, Ft, dFt, a, Fa, dFa, b);
   }
   return a;
 }
 
-// Alg. 3 lines 2-9: t_p, g(t_p), t0, t1 in type M::T.
-// The regime test g''(0) = v^2 - x > 0 is taken in double on the
-// caller's inputs.  Returns false when FindRange hits its cap.
-template <class M>
-__device__ __forceinline__ bool make_plan(double vd, double xd, double log_eps,
-                                          typename M::T &tp, typename M::T &gp,
-                                          typename M::T &t0, typename M::T &t1) {
-  using T = typename M::T;
-  const T v = T(vd), x = T(xd);
-  const T hx = T(0.5) * x;
-  const T ones = M::scale(T(1));
-  const T m2vs = M::scale(T(-2) * v);
-  const T L = T(log_eps);
-  T lo, hi, Fh, dFh;
-  tp = T(0);
-  if (vd * vd - xd > 0.0) {
-    PeakFn<M> pf{v, hx, v * v, m2vs, ones};
-    if (!find_range(pf, T(0), lo, hi, Fh, dFh)) return false;
-    tp = find_zero<M>(pf, hi, Fh, dFh, lo);       // (t_e, t_s)
+__device__ __forceinline__ Plan<double> make_plan_f64(double v, double x, double log_eps) {
+  Plan<double> p;
+  PlanF64 P{v, x, 0.5 * x, v * v, -2.0 * v};
+  double lo, hi, Fh, dFh;
+  p.ok = false;
+  p.tp = 0.0;
+  auto pf = [&](double t, double &F, double &dF) { P.peak(t, F, dF); };
+  if (v * v - x > 0.0) {
+    if (!find_range(pf, 0.0, lo, hi, Fh, dFh)) return p;
+    p.tp = find_zero_f64(pf, hi, Fh, dFh, lo);
   }
-  gp = g_value<M>(v, hx, m2vs, ones, tp);
-  ThreshFn<M> df{v, hx, m2vs, ones, gp + L + T(kLn2)};
-  t0 = T(0);
-  const T d0 = -x - gp - L;                       // d(0) = g(0) - g(t_p) - log eps
-  if (d0 <= T(0)) t0 = find_zero<M>(df, T(0), d0, T(0), tp);   // P:262-265, g'(0) = 0
-  if (!find_range(df, tp, lo, hi, Fh, dFh)) return false;
-  t1 = find_zero<M>(df, hi, Fh, dFh, lo);
-  return true;
+  p.gp = P.gval(p.tp);
+  const double c = p.gp + log_eps + kLn2;
+  auto df = [&](double t, double &F, double &dF) { P.thr(c, t, F, dF); };
+  p.t0 = 0.0;
+  double d0 = -x - p.gp - log_eps;
+  if (d0 <= 0.0) p.t0 = find_zero_f64(df, 0.0, d0, 0.0, p.tp);
+  if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
+  p.t1 = find_zero_f64(df, hi, Fh, dFh, lo);
+  p.dmin = fmin(d0, Fh);
+  p.ok = true;
+  return p;
 }
 
 // Inputs for which the FP32 range finder is used under BLK_RANGE_AUTO:
