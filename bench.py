@@ -59,7 +59,24 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--out", default="")
+    p.add_argument("--strong", action="store_true",
+                   help="shard the config's batch over the ranks (default for c5)")
     return p.parse_args()
+
+
+def _generate_chunked(cfg, start, count, total):
+    """Inputs [start, start+count) in 2^24-element pieces (bounded host memory)."""
+    import numpy as _np
+    parts_v, parts_x = [], []
+    step = 1 << 24
+    for s0 in range(start, start + count, step):
+        m = min(step, start + count - s0)
+        v, x = workloads.generate(cfg, s0, m, n=total)
+        parts_v.append(v)
+        parts_x.append(x)
+    if not parts_v:
+        return workloads.generate(cfg, 0, 0, n=max(total, 1))
+    return _np.concatenate(parts_v), _np.concatenate(parts_x)
 
 
 def cpu_info():
@@ -166,7 +183,8 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": "logK+dv+dx evals/sec FP64", "value": value,
         "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": n_used / value * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": n_used / value * 1e3, "higher_is_better": True,
+        "scaling": "strong" if (args.strong or args.config == "c5") else "weak",
         "vs_baseline": None, "dtype": "f64" if c.precision == "f64" else "f32",
         "data": "synthetic (seeded, BASELINE.json config)",
         "config": {"workload": args.config, "describe": c.describe, "nbins": args.nbins,
@@ -197,9 +215,21 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     c = workloads.CONFIGS[args.config]
-    n = args.n or c.n
     dt = torch.float64 if c.precision == "f64" else torch.float32
-    v_np, x_np = workloads.generate(args.config, rank * n, n, n=n * world)
+    from paper_2108_11560_b200.dist import shard_range
+    if args.strong or args.config == "c5":
+        # strong scaling: the config's whole batch, contiguous shards (c5: 2^28 over N GPUs)
+        scaling = "strong"
+        total = args.n or c.n
+        lo, hi = shard_range(total, world, rank)
+    else:
+        # weak scaling: every rank its own batch of the config's size
+        scaling = "weak"
+        per = args.n or c.n
+        total = per * world
+        lo, hi = rank * per, (rank + 1) * per
+    n = hi - lo
+    v_np, x_np = _generate_chunked(args.config, lo, n, total)
     v = torch.from_numpy(v_np).to(dev)
     x = torch.from_numpy(x_np).to(dev)
     outs = {k: (torch.empty(n, dtype=dt, device=dev) if k in c.outputs else None)
@@ -255,7 +285,7 @@ def main():
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_ms = float(total_ms.item())
     ms_per_step = total_ms / args.steps
-    value = n * world * args.steps / (total_ms * 1e-3)
+    value = total * args.steps / (total_ms * 1e-3)
 
     # end to end through the host-buffer C-ABI entry point (FP64 configs)
     e2e = None
@@ -287,7 +317,7 @@ def main():
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         e2e_launches = args.steps * ((n + chunk - 1) // chunk)
-        e2e = {"value": n * world * args.steps / (float(e2e_ms.item()) * 1e-3), "unit": "evals/s",
+        e2e = {"value": total * args.steps / (float(e2e_ms.item()) * 1e-3), "unit": "evals/s",
                "h2d_bytes_per_step": 2 * n * 8,
                "d2h_bytes_per_step": len(c.outputs) * n * 8,
                "path": "bessel_logk_f64_host (pinned host buffers, 2^18-element chunks on 3 streams)"}
@@ -328,9 +358,10 @@ def main():
         "metric": "logK+dv+dx evals/sec FP64" if dt == torch.float64 else "logK+dv+dx evals/sec FP32",
         "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dt == torch.float64 else "f32",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64" if dt == torch.float64 else "f32",
         "data": "synthetic (seeded numpy PCG64 blocks, BASELINE.json config distribution)",
-        "config": {"workload": args.config, "describe": c.describe, "elements_per_gpu": n,
+        "config": {"workload": args.config, "describe": c.describe, "elements_total": total,
+                   "elements_per_gpu": n,
                    "nbins": args.nbins, "outputs": list(c.outputs),
                    "l2": "flushed between timed steps (512 MiB write, outside events)",
                    "parallelism": f"dp{world} (contiguous element shards, no collective)"},
