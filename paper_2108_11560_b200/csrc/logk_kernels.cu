@@ -45,10 +45,9 @@ __global__ void __launch_bounds__(128, BLK_MINB)
 logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 double *__restrict__ logk, double *__restrict__ dlogk_dv,
                 double *__restrict__ dlogk_dx, int nbins, int range_mode) {
-  __shared__ double tab_s[kTabSize];
-  load_exp_table(tab_s);
+  load_exp_table();
   __syncthreads();
-  const double *tab = lane_table(tab_s);
+  const double *tab = g_exp_tab;
 
   const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t i = gtid / LPE;

@@ -21,7 +21,8 @@
 
 namespace blk {
 
-constexpr int kExpTab = 256;      // 2^(j/256), j = 0..255, in shared memory
+constexpr int kExpBits = 11;
+constexpr int kExpTab = 1 << kExpBits;   // 2^(j/2048), j = 0..2047, in shared memory (16 KB)
 #ifndef BLK_TAB_REP
 #define BLK_TAB_REP 1
 #endif
@@ -32,7 +33,7 @@ constexpr int kExpTab = 256;      // 2^(j/256), j = 0..255, in shared memory
 // fill costs more, so the default is a single copy.
 constexpr int kTabRep = BLK_TAB_REP;
 constexpr int kTabSize = kExpTab * kTabRep;
-constexpr int kAnchor = 36;       // FP64 re-anchoring interval for e^{+-t} (max)
+constexpr int kAnchor = 44;       // FP64 re-anchoring interval for e^{+-t} (max)
 #ifndef BLK_GROUP
 #define BLK_GROUP 4
 #endif
@@ -49,29 +50,61 @@ constexpr bool kAcc2 = BLK_ACC2;  // split the sums over two accumulator sets
 #endif
 constexpr bool kLockstep = BLK_LOCKSTEP;  // stage-by-stage evaluation of a group
 
-__device__ const double kExp2Table[kExpTab] = {
+__device__ __align__(16) const double kExp2Table[kExpTab] = {
 #include "exp2_table.inc"
 };
 
-// Block-cooperative copy of the table to shared memory (caller syncs).
-// tab has kTabSize doubles.
-__device__ __forceinline__ void load_exp_table(double *tab) {
-  for (int j = threadIdx.x; j < kTabSize; j += blockDim.x) tab[j] = kExp2Table[j / kTabRep];
-}
-// This lane's copy of the table (pass the result to exp_tab).
-__device__ __forceinline__ const double *lane_table(const double *tab) {
-  return tab + (threadIdx.x % kTabRep);
-}
+// The shared-memory copy of the table, one per CTA of every kernel that
+// uses exp_tab.  A file-scope __shared__ array lets LDS address it with an
+// immediate offset (no base-register add per node).
+__shared__ __align__(16) double g_exp_tab[kTabSize];
 
-// exp(a) by Tang's table method: a = (k/256) ln2 + r, |r| <= ln2/512,
-// exp(a) = 2^(k>>8) * T[k&255] * (1 + r + r^2/2 + r^3/6 + r^4/24).
-// Valid for a in [-707, 709]; CLAMP maps a < -707 to e^-707 (caller decides
-// whether its arguments can leave the range -- see quad_f64).
-// 8 FP64-pipe instructions + 1 LDS.64 + 5 integer ops.
-constexpr double kExpInvL = 369.3299304675746;       // 256 / ln 2
+// Block-cooperative copy of the table to shared memory (caller syncs).
+__device__ __forceinline__ void load_exp_table(double *tab = g_exp_tab) {
+  if (kTabRep == 1) {
+    const double2 *src = reinterpret_cast<const double2 *>(kExp2Table);
+    double2 *dst = reinterpret_cast<double2 *>(tab);
+    for (int j = threadIdx.x; j < kExpTab / 2; j += blockDim.x) dst[j] = src[j];
+  } else {
+    for (int j = threadIdx.x; j < kTabSize; j += blockDim.x) tab[j] = kExp2Table[j / kTabRep];
+  }
+}
+// Table entry j for this lane (copy threadIdx.x % kTabRep): one LOP3 for
+// the caller's mask, one IMAD for the byte address, one LDS.64.
+__device__ __forceinline__ double exp_table_entry(int j) {
+  if (kTabRep != 1) return g_exp_tab[j * kTabRep + (int)(threadIdx.x % kTabRep)];
+  const unsigned base = (unsigned)__cvta_generic_to_shared(g_exp_tab);
+  unsigned addr;
+  asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(addr) : "r"((unsigned)j), "r"(base));
+  double val;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(val) : "r"(addr) : "memory");
+  return val;
+}
+// Kept for call sites that pass a table pointer; the shared table is global.
+__device__ __forceinline__ const double *lane_table(const double *tab) { return tab; }
+
+// exp(a) by Tang's table method: a = (k/2048) ln2 + r, |r| <= ln2/4096,
+// exp(a) = 2^(k>>11) * T[k&2047] * (1 + r + r^2/2 + r^3/6)   (truncation
+// r^4/24 < 3.5e-17).  Valid for a in [-707, 709]; CLAMP maps a < -707 to
+// e^-707 (caller decides whether its arguments can leave the range -- see
+// quad_f64).  7 FP64-pipe instructions + 1 LDS.64 + 4 integer ops.
+// hi + (n << 20) as one integer multiply-add (ptxas would otherwise rewrite
+// (k >> 11) << 20 as (k << 9) & mask and add: three instructions).
+__device__ __forceinline__ int add_exponent(int hi, int n) {
+  int r;
+  asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(r) : "r"(n), "r"(hi));
+  return r;
+}
+constexpr double kExpInvL = 2954.639443740597;       // 2048 / ln 2
 constexpr double kExpMagic = 6755399441055744.0;     // 1.5 * 2^52: round-to-int trick
-constexpr double kExpC = 0.0027076061740622863;      // ln2/256 (single-step reduction:
-                                                     // |k| <= 2^18 -> |error| < 1.2e-13 |a|/707)
+constexpr double kExpC = 0.0003384507717577858;      // ln2/2048 (single-step reduction:
+                                                     // |k| <= 2.1e6 -> |error| < 6e-14 |a|/707)
+__device__ __forceinline__ double exp_poly_scale(double r, int k, double tj) {
+  double p = fma(r, 1.6666666666666666e-01, 0.5);
+  p = fma(p, r * r, r);                               // e^r - 1
+  const double res = fma(tj, p, tj);
+  return __hiloint2double(add_exponent(__double2hiint(res), k >> kExpBits), __double2loint(res));
+}
 template <bool CLAMP>
 __device__ __forceinline__ double exp_tab(double a, const double *__restrict__ tab) {
   if (CLAMP) a = a < -707.0 ? -707.0 : a;
@@ -79,13 +112,8 @@ __device__ __forceinline__ double exp_tab(double a, const double *__restrict__ t
   const int k = __double2loint(kd);
   kd -= kExpMagic;
   const double r = fma(kd, -kExpC, a);
-  double p = fma(r, 4.1666666666666666e-02, 1.6666666666666666e-01);
-  p = fma(p, r, 0.5);
-  p = fma(p, r * r, r);                               // e^r - 1
-  const double tj = tab[(k & (kExpTab - 1)) * kTabRep];
-  const double res = fma(tj, p, tj);
-  const int hi = __double2hiint(res) + ((k >> 8) << 20);
-  return __hiloint2double(hi, __double2loint(res));
+  (void)tab;
+  return exp_poly_scale(r, k, exp_table_entry(k & (kExpTab - 1)));
 }
 
 // 1/a to ~1 ulp: MUFU.RCP64H seed + two Newton steps.
@@ -203,19 +231,18 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
         for (int j = 0; j < kGroup; ++j) { k[j] = __double2loint(kd[j]); kd[j] -= kExpMagic; }
         double tj[kGroup];
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) tj[j] = tab[(k[j] & (kExpTab - 1)) * kTabRep];
+        for (int j = 0; j < kGroup; ++j) tj[j] = exp_table_entry(k[j] & (kExpTab - 1));
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) pp[j] = fma(r[j], 4.1666666666666666e-02, 1.6666666666666666e-01);
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j], 0.5);
+        for (int j = 0; j < kGroup; ++j) pp[j] = fma(r[j], 1.6666666666666666e-01, 0.5);
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j] * r[j], r[j]);
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) {
           const double res = fma(tj[j], pp[j], tj[j]);
-          E[j] = __hiloint2double(__double2hiint(res) + ((k[j] >> 8) << 20), __double2loint(res));
+          E[j] = __hiloint2double(add_exponent(__double2hiint(res), k[j] >> kExpBits),
+                                  __double2loint(res));
         }
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) {

@@ -126,13 +126,20 @@ __device__ __forceinline__ void fz_points(T a, T Fa, T dFa, T b, T &mid, T &tn) 
   T lo = fmin(a, mid), hi = fmax(a, mid);        // Clip to [a, mid] (R3)
   tn = fmin(fmax(t, lo), hi);
 }
+// FP32 variant with the search direction known at compile time: ASC (t0
+// search, a = 0 < b = t_p) or descending (peak and t1 searches, a > b).  The
+// clip to [a, mid] then needs two min/max, and a non-finite Newton point
+// lands on mid through the NaN rules of fminf/fmaxf: NaN -> mid; +inf (only
+// from F'(a) = +0, i.e. the first t0 step, R18) -> mid in the ascending
+// search; -inf (F'(a) = -0) -> mid in the descending ones.  The remaining
+// infinities (-inf ascending, +inf descending) need F(a)/F'(a) of the
+// wrong sign, which the bracket invariants exclude.
+template <bool ASC>
 __device__ __forceinline__ void fz_points_f32(float a, float Fa, float dFa, float b, float &mid,
                                               float &tn) {
-  mid = a + (b - a) * 0.5f;
-  float t = a - Fa * rcp_approx(dFa);
-  t = isfinite(t) ? t : mid;
-  float lo = fminf(a, mid), hi = fmaxf(a, mid);
-  tn = fminf(fmaxf(t, lo), hi);
+  mid = fmaf(b - a, 0.5f, a);
+  const float t = fmaf(-Fa, rcp_approx(dFa), a);
+  tn = ASC ? fmaxf(fminf(t, mid), a) : fminf(fmaxf(t, mid), a);
 }
 
 // ... then the three-way bracket update, branch-free.
@@ -150,13 +157,13 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 }
 
 // Alg. 2 with the two evaluations packed into f32x2 operations.
-template <bool PEAK>
+template <bool PEAK, bool ASC>
 __device__ __forceinline__ float find_zero_f32(const PlanF32 &P, float c, float a, float &Fa,
                                                float dFa, float b) {
 #pragma unroll 1
   for (int i = 0; i < kMaxIter; ++i) {
     float mid, tn;
-    fz_points_f32(a, Fa, dFa, b, mid, tn);
+    fz_points_f32<ASC>(a, Fa, dFa, b, mid, tn);
     float2 F, dF;
     if (PEAK) P.peak2(f2(mid, tn), F, dF);
     else P.thr2(c, f2(mid, tn), F, dF);
@@ -197,16 +204,16 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   if (vd * vd - xd > 0.0) {
     auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
     if (!find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
-    p.tp = find_zero_f32<true>(P, 0.0f, hi, Fh, dFh, lo);         // (t_e, t_s)
+    p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo);  // (t_e, t_s)
   }
   p.gp = P.gval(p.tp);
   const float c = p.gp + P.L + float(kLn2);
   p.t0 = 0.0f;
   float d0 = -P.x - p.gp - P.L;                                    // d(0)
-  if (d0 <= 0.0f) p.t0 = find_zero_f32<false>(P, c, 0.0f, d0, 0.0f, p.tp);
+  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp);
   auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
   if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
-  p.t1 = find_zero_f32<false>(P, c, hi, Fh, dFh, lo);
+  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo);
   p.dmin = fminf(d0, Fh);
   p.ok = true;
   return p;

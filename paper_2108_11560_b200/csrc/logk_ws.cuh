@@ -46,7 +46,6 @@ struct SlotLane {
 };
 
 struct WsShared {
-  double tab[kTabSize];
   SlotLane slot[kSlots][32];
   unsigned long long full[kSlots];
   unsigned long long empty[kSlots];
@@ -81,7 +80,7 @@ logk_f64_ws_kernel(const double *__restrict__ vin, const double *__restrict__ xi
   extern __shared__ __align__(16) unsigned char ws_raw[];
   WsShared &S = *reinterpret_cast<WsShared *>(ws_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  load_exp_table(S.tab);
+  load_exp_table();
   if (threadIdx.x < kSlots) {
     mbar_init(&S.full[threadIdx.x], 32);
     mbar_init(&S.empty[threadIdx.x], 32);
@@ -145,9 +144,9 @@ logk_f64_ws_kernel(const double *__restrict__ vin, const double *__restrict__ xi
       Sums64 r{0.0, 0.0, 0.0};
       if (ok) {
         if (!(sl.flags & 2))
-          r = quad_f64<DV, DX, false>(sl.v, sl.x, sl.t0, sl.h, sl.gp, nbins, 0, nbins + 1, lane_table(S.tab));
+          r = quad_f64<DV, DX, false>(sl.v, sl.x, sl.t0, sl.h, sl.gp, nbins, 0, nbins + 1, g_exp_tab);
         else
-          r = quad_f64<DV, DX, true>(sl.v, sl.x, sl.t0, sl.h, sl.gp, nbins, 0, nbins + 1, lane_table(S.tab));
+          r = quad_f64<DV, DX, true>(sl.v, sl.x, sl.t0, sl.h, sl.gp, nbins, 0, nbins + 1, g_exp_tab);
       }
       if (i < n_el) {
         const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
