@@ -75,7 +75,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   }
   // a6: fixed-bin quadrature, three sums in one pass
   Sums64 s{0.0, 0.0, 0.0};
-  const double h = (t1 - t0) / nbins;
+  const double h = (t1 - t0) * rcp64((double)nbins);   // h = (t1 - t0)/n
   if (ok) {
     int mb, me;
     lane_bins<LPE>(nbins, sub, mb, me);

@@ -33,7 +33,10 @@ constexpr int kExpTab = 1 << kExpBits;   // 2^(j/2048), j = 0..2047, in shared m
 // fill costs more, so the default is a single copy.
 constexpr int kTabRep = BLK_TAB_REP;
 constexpr int kTabSize = kExpTab * kTabRep;
-constexpr int kAnchor = 44;       // FP64 re-anchoring interval for e^{+-t} (max)
+#ifndef BLK_ANCHOR
+#define BLK_ANCHOR 44
+#endif
+constexpr int kAnchor = BLK_ANCHOR; // FP64 re-anchoring interval for e^{+-t} (nodes)
 #ifndef BLK_GROUP
 #define BLK_GROUP 4
 #endif
@@ -49,6 +52,10 @@ constexpr bool kAcc2 = BLK_ACC2;  // split the sums over two accumulator sets
 #define BLK_LOCKSTEP 1
 #endif
 constexpr bool kLockstep = BLK_LOCKSTEP;  // stage-by-stage evaluation of a group
+#ifndef BLK_I2F
+#define BLK_I2F 0
+#endif
+constexpr bool kI2F = BLK_I2F;    // k as double by I2F.F64 instead of kd - magic
 
 __device__ __align__(16) const double kExp2Table[kExpTab] = {
 #include "exp2_table.inc"
@@ -181,9 +188,9 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
   const double a1 = DV ? one_minus_exp(m2v * h, tab) : 0.0;
   double S0 = 0.0, S1 = 0.0, S2 = 0.0;
   double T0 = 0.0, T1 = 0.0, T2 = 0.0;               // second accumulator set (kAcc2)
-  // chunks of <= kAnchor nodes, equal sizes rounded up to whole groups
-  const int nch = (ie - ib + kAnchor - 1) / kAnchor;
-  const int csz = ((ie - ib + nch - 1) / nch + kGroup - 1) / kGroup * kGroup;
+  // chunks of kAnchor nodes (a multiple of kGroup), the last one shorter
+  constexpr int csz = kAnchor;
+  static_assert(kAnchor % kGroup == 0, "anchor interval must hold whole groups");
 #pragma unroll 1
   for (int c0 = ib; c0 < ie; c0 += csz) {
     const int c1 = min(c0 + csz, ie);
@@ -228,7 +235,10 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) kd[j] = fma(a[j], kExpInvL, kExpMagic);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) { k[j] = __double2loint(kd[j]); kd[j] -= kExpMagic; }
+        for (int j = 0; j < kGroup; ++j) {
+          k[j] = __double2loint(kd[j]);
+          kd[j] = kI2F ? __int2double_rn(k[j]) : kd[j] - kExpMagic;
+        }
         double tj[kGroup];
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) tj[j] = exp_table_entry(k[j] & (kExpTab - 1));

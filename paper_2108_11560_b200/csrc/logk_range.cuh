@@ -160,7 +160,7 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 template <bool PEAK, bool ASC>
 __device__ __forceinline__ float find_zero_f32(const PlanF32 &P, float c, float a, float &Fa,
                                                float dFa, float b) {
-#pragma unroll 1
+#pragma unroll 2
   for (int i = 0; i < kMaxIter; ++i) {
     float mid, tn;
     fz_points_f32<ASC>(a, Fa, dFa, b, mid, tn);

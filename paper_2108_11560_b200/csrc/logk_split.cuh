@@ -37,7 +37,7 @@ plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
   PlanRec r;
-  r.t0 = t0; r.h = (t1 - t0) / nbins; r.gp = gp;
+  r.t0 = t0; r.h = (t1 - t0) * rcp64((double)nbins); r.gp = gp;
   r.flags = (ok ? 1 : 0) | (dmin > -600.0 ? 0 : 2) | (vraw < 0.0 ? 4 : 0);
   r.pad = 0;
   plans[i] = r;

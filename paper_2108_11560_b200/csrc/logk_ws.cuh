@@ -121,7 +121,7 @@ logk_f64_ws_kernel(const double *__restrict__ vin, const double *__restrict__ xi
       }
       SlotLane &sl = S.slot[s][lane];
       sl.t0 = t0;
-      sl.h = (t1 - t0) / nbins;
+      sl.h = (t1 - t0) * rcp64((double)nbins);
       sl.gp = gp;
       sl.v = v;
       sl.x = x;
