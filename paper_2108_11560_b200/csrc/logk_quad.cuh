@@ -347,43 +347,132 @@ __device__ __forceinline__ float exp_split_f32(float a) {
   return fmaf(e, yl * 0.6931471805599453f, e);
 }
 
+// 1/a for a in a normal range without MUFU: magic-constant seed (12%) and
+// three Newton steps (-> ~1 ulp).  Used where the kernel is MUFU-bound.
+__device__ __forceinline__ float2 rcp_newton2(float2 a) {
+  float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(a.x)),
+                         __int_as_float(0x7EF311C3 - __float_as_int(a.y)));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) y = mul2(y, fma2(mul2(a, f2s(-1.0f)), y, f2s(2.0f)));
+  return y;
+}
+
+// FP32 entry point quadrature.  The weight exponent g(t) - s is a difference
+// of terms as large as v t and x cosh t (~1e2 in config 4) whose FP32
+// rounding (~1e-5 absolute) would reach the 1e-5 tolerance on log K near
+// |log K| ~ 1 (measured by emulation: 9e-6 with FP32 recurrences for
+// cosh t).  So the node position, cosh t and the exponent are formed in FP64
+// (6 FP64 instructions per node) and rounded once to FP32, where MUFU.EX2
+// takes the exponential; the weights, q, p and the three sums are FP32, the
+// sums blocked every 16 nodes into FP64 (error ~1e-7 ~ eps32).
+// double -> float by truncation with three integer ops (IADD, SHF.L.U64,
+// LOP3) instead of F2F.F32.F64, which runs on the XU pipe next to MUFU and
+// made the FP32 kernel XU-bound.  Valid for |d| in [2^-100, 2^127]; smaller
+// magnitudes give 0 (a weight exponent of 0 +- 2^-100 is 1 to FP32 anyway).
+__device__ __forceinline__ float d2f_trunc(double d) {
+  const int hi = __double2hiint(d), lo = __double2loint(d);
+  const int b = hi - 0x38000000;                        // rebias exponent 1023 -> 127
+  int f;
+  asm("shf.l.clamp.b32 %0, %1, %2, 3;" : "=r"(f) : "r"(lo), "r"(b));   // (b << 3) | (lo >> 29)
+  f = (f & 0x7fffffff) | (hi & 0x80000000);
+  return (hi & 0x7ff00000) < 0x39b00000 ? 0.0f : __int_as_float(f);
+}
+
 template <bool DV, bool DX>
-__device__ __forceinline__ Sums32 quad_f32(float v, float x, float t0, float h, float shift,
+__device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float hf, float shift,
                                            int n, int mb, int me) {
-  Sums32 s{0.0f, 0.0f, 0.0f};
-  const float kL2e = 1.4426950408889634f;
-  const float s_mid = shift + 0.6931471805599453f;
-  const float s_end = s_mid + 0.6931471805599453f;
-  const float m2v = -2.0f * v;
-  const float a1 = -expm1f(m2v * h);
-  float p = -expm1f(m2v * fmaf((float)mb, h, t0));
-  float mf = (float)mb;
-  // partial sums per block of 16 nodes keep FP32 accumulation error small
-  Sums32 blk{0.0f, 0.0f, 0.0f};
-  int inblk = 0;
-#pragma unroll 2
-  for (int m = mb; m < me; ++m) {
-    const float t = fmaf(mf, h, t0);
-    const float e = exp_split_f32(t);
-    const float ch = 0.5f * (e + rcp_approx(e));
-    const float q = ex2_approx(m2v * kL2e * t);
-    const float sm = (m == 0 || m == n) ? s_end : s_mid;
-    const float arg = fmaf(-x, ch, fmaf(v, t, -sm));
-    const float E = ex2_approx(arg * kL2e);
-    const float w = fmaf(E, q, E);
-    blk.S0 += w;
-    if (DX) blk.S2 = fmaf(w, ch, blk.S2);
-    if (DV) blk.S1 = fmaf(E * t, p, blk.S1);
-    if (DV) p = fmaf(q, a1, p);
-    mf += 1.0f;
-    if (++inblk == 16) {
-      s.S0 += blk.S0; s.S1 += blk.S1; s.S2 += blk.S2;
-      blk = Sums32{0.0f, 0.0f, 0.0f};
-      inblk = 0;
+  const double kLog2e = 1.4426950408889634;
+  const double v = vf, x = xf, t0 = t0f, h = hf;
+  // exponent in log2 units: a2 = (v t - x cosh t - s - log 2) log2(e)
+  const double v2 = v * kLog2e, nx2 = -x * kLog2e;
+  const double ns2 = -((double)shift + kLn2) * kLog2e;
+  const double eh = exp(h), ehi = rcp64(eh);
+  const float ehf = float(eh), ehif = float(ehi);
+  const float m2vl = float(-2.0 * v2);
+  const float eqf = ex2_approx(m2vl * hf);
+  const float a1 = -expm1f(-2.0f * vf * hf);
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+  static_assert(kAnchor % 4 == 0, "anchor interval must hold whole groups");
+#pragma unroll 1
+  for (int c0 = mb; c0 < me; c0 += kAnchor) {
+    const int c1 = min(c0 + kAnchor, me);
+    double tc = fma((double)c0, h, t0);
+    double et = 0.5 * exp(tc), eti = 0.25 * rcp64(et);
+    const float tcf = float(tc);
+    // FP32 copies of t and e^{+-t}/2 for the products (weights only)
+    float etf = float(et), etif = float(eti);
+    float q = ex2_approx(m2vl * tcf);                      // q, p re-anchored per chunk
+    float p = -expm1f(-2.0f * vf * tcf);
+    float B0 = 0.0f, B1 = 0.0f, B2 = 0.0f;                 // per-chunk FP32 partial sums
+    int m = c0;
+    float jf = 0.0f;
+#pragma unroll 1
+    for (; m + 4 <= c1; m += 4) {
+      double ch[4], tt[4];
+      float E[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        tt[j] = j == 0 ? tc : fma(double(j), h, tc);
+        ch[j] = et + eti;
+        et *= eh;
+        eti *= ehi;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) E[j] = ex2_approx(d2f_trunc(fma(nx2, ch[j], fma(v2, tt[j], ns2))));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float chf = etf + etif;
+        const float tf = fmaf(jf + float(j), hf, tcf);
+        const float w = fmaf(E[j], q, E[j]);               // E (1 + q)
+        B0 += w;
+        if (DX) B2 = fmaf(w, chf, B2);
+        if (DV) {
+          B1 = fmaf(E[j] * tf, p, B1);
+          p = fmaf(q, a1, p);
+        }
+        q *= eqf;
+        etf *= ehf;
+        etif *= ehif;
+      }
+      jf += 4.0f;
+      tc = fma((double)(m + 4), h, t0);
     }
+#pragma unroll 1
+    for (; m < c1; ++m) {
+      const double t = fma((double)m, h, t0);
+      const double ch = et + eti;
+      et *= eh;
+      eti *= ehi;
+      const float E = ex2_approx(d2f_trunc(fma(nx2, ch, fma(v2, t, ns2))));
+      const float w = fmaf(E, q, E);
+      B0 += w;
+      if (DX) B2 = fmaf(w, etf + etif, B2);
+      if (DV) {
+        B1 = fmaf(E * float(t), p, B1);
+        p = fmaf(q, a1, p);
+      }
+      q *= eqf;
+      etf *= ehf;
+      etif *= ehif;
+    }
+    S0 += B0; S1 += B1; S2 += B2;
   }
-  s.S0 += blk.S0; s.S1 += blk.S1; s.S2 += blk.S2;
-  return s;
+  // half weights of nodes 0 and n, evaluated directly
+  auto half_node = [&](int mm) {
+    const double t = fma((double)mm, h, t0);
+    const double et = 0.5 * exp(t);
+    const double ch = et + 0.25 * rcp64(et);
+    const float E = 0.5f * ex2_approx(float(fma(nx2, ch, fma(v2, t, ns2))));
+    const float tf = float(t);
+    const float q1 = ex2_approx(m2vl * tf);
+    const float w = fmaf(E, q1, E);
+    S0 -= w;
+    if (DX) S2 -= double(w) * float(ch);
+    if (DV) S1 -= double(E * tf) * (-expm1f(-2.0f * vf * tf));
+  };
+  if (mb == 0) half_node(0);
+  if (me == n + 1) half_node(n);
+  return Sums32{float(S0), float(S1), float(S2)};
 }
 
 }  // namespace blk

@@ -64,8 +64,33 @@ struct Plan {
   bool ok;
 };
 
+// 1/(1+q) for q in [0,1] without MUFU: linear seed on [1,2] (max error 6%)
+// and three Newton steps (6e-8).  Used by the FP32 entry point, whose range
+// finding is MUFU-bound; the FP64 kernel is issue-bound and keeps MUFU.RCP.
+__device__ __forceinline__ float2 rcp_1pq2(float2 opq) {
+  float2 r = fma2(opq, f2s(-0.5f), f2s(1.4571f));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r = mul2(r, fma2(mul2(opq, f2s(-1.0f)), r, f2s(2.0f)));
+  return r;
+}
+
+// e^{-t} = 1/e^t without MUFU: magic-constant seed, three Newton steps; e^t
+// beyond 2^120 (t > 83, only FindRange probes get there) maps to 0.
+// (Measured slower than MUFU.RCP in the FP32 kernel -- it turns it
+// issue-bound -- so it is not used; kept for reference.)
+__device__ __forceinline__ float2 rcp_exp2(float2 e) {
+  float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(e.x)),
+                         __int_as_float(0x7EF311C3 - __float_as_int(e.y)));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) y = mul2(y, fma2(mul2(e, f2s(-1.0f)), y, f2s(2.0f)));
+  y.x = e.x > 1.3e36f ? 0.0f : y.x;
+  y.y = e.y > 1.3e36f ? 0.0f : y.y;
+  return y;
+}
+
 // ============================================================== FP32 (packed)
-struct PlanF32 {
+template <bool NEWTON>
+struct PlanF32T {
   static constexpr float kL2e = 1.4426950408889634f;
   static constexpr float kLn2f = 0.6931471805599453f;
   float v, x, hx, v2, m2vs, L;
@@ -82,7 +107,7 @@ struct PlanF32 {
     float2 e = ex2_2(mul2(t, f2s(kL2e)));
     float2 ei = rcp_2(e);
     float2 q = ex2_2(mul2(t, f2s(m2vs)));
-    float2 r = rcp_2(add2(q, f2s(1.0f)));
+    float2 r = NEWTON ? rcp_1pq2(add2(q, f2s(1.0f))) : rcp_2(add2(q, f2s(1.0f)));
     float2 th = mul2(add2(f2s(1.0f), mul2(q, f2s(-1.0f))), r);
     float2 s2 = mul2(mul2(q, f2s(4.0f)), mul2(r, r));
     F = fma2(f2s(v), th, mul2(f2s(-hx), add2(e, mul2(ei, f2s(-1.0f)))));
@@ -101,7 +126,7 @@ struct PlanF32 {
     float2 ei = rcp_2(e);
     float2 q = ex2_2(mul2(t, f2s(m2vs)));
     float2 opq = add2(q, f2s(1.0f));
-    float2 r = rcp_2(opq);
+    float2 r = NEWTON ? rcp_1pq2(opq) : rcp_2(opq);
     float2 lq = lg2_2(opq);
     float2 base = fma2(lq, f2s(kLn2f), f2s(-c));
     base = fma2(f2s(v), t, base);
@@ -156,9 +181,11 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
   a = na; Fa = nFa; dFa = ndFa;
 }
 
+using PlanF32 = PlanF32T<false>;
+
 // Alg. 2 with the two evaluations packed into f32x2 operations.
-template <bool PEAK, bool ASC>
-__device__ __forceinline__ float find_zero_f32(const PlanF32 &P, float c, float a, float &Fa,
+template <bool PEAK, bool ASC, class PF>
+__device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
                                                float dFa, float b) {
 #pragma unroll 2
   for (int i = 0; i < kMaxIter; ++i) {
@@ -193,11 +220,12 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 
 // Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
 // is taken in double on the caller's inputs.
+template <bool NEWTON = false>
 __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps) {
   Plan<float> p;
-  PlanF32 P;
+  PlanF32T<NEWTON> P;
   P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
-  P.m2vs = -2.0f * P.v * PlanF32::kL2e; P.L = float(log_eps);
+  P.m2vs = -2.0f * P.v * PlanF32T<NEWTON>::kL2e; P.L = float(log_eps);
   float lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0f;
