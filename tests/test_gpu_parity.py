@@ -270,3 +270,25 @@ def test_microbenchmarks_run():
     torch.cuda.synchronize()
     assert ops == 148 * 256 * 10 * 16
     assert bool(torch.isfinite(out).all())
+
+
+# --------------------------------------------- the paper's own experiments
+def test_paper_accuracy_grid():
+    """Sec. 3.1: on v = 0..99 x x = 10^-1..10^2.1 (100 x 33) the
+    error metric log10(|Delta|/eps + 1) against the plain definition
+    (long-double brute force) has no region >= 4 (the paper's cut for an
+    inaccurate region) and a mean below 1 for log K and dx; FP32
+    (eps = 2^-23) likewise ('less than 1 eps in most regions', P:425-426)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "paper_experiments", os.path.join(os.path.dirname(__file__), "..", "tools",
+                                          "paper_experiments.py"))
+    pe = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(pe)
+    res = pe.accuracy_grid(128)
+    for name in ("gpu_f64", "gpu_f32"):
+        for k in ("logk", "dx", "dv"):
+            assert res[name][k]["cells_ge_4"] == 0, (name, k, res[name][k])
+        assert res[name]["logk"]["mean"] < 1.0, res[name]
+        assert res[name]["dx"]["mean"] < 1.0, res[name]

@@ -47,6 +47,10 @@ CONFIGS = {
                  "2^26 pairs FP32, v~U[0,50], x~logU[1e-2,1e2]"),
     "c5": Config("c5", 5, 1 << 28, "f64", ("logk", "dx"),
                  "2^28 pairs FP64 NIG batch, v~{1,.5,2.5,5}, x=a*sqrt(d^2+y^2)"),
+    # the paper's own batch-size experiment (Sec. 3.4, Fig. 5):
+    # v = 10^(2r) - 1 in [0, 99], x = 10^(3r - 1) in [0.1, 100], r ~ U(0,1)
+    "fig5": Config("fig5", 6, 1 << 28, "f64", ("logk", "dv", "dx"),
+                   "paper Fig. 5 distribution: v=10^(2r)-1, x=10^(3r-1), r~U(0,1)"),
 }
 
 
@@ -70,6 +74,10 @@ def _block(cfg: Config, b: int, count: int, seed: int):
     elif k == "c4":
         v = rng.uniform(0.0, 50.0, count)
         x = _logu(rng, 1e-2, 1e2, count)
+    elif k == "fig5":
+        r = rng.uniform(0.0, 1.0, count)
+        v = 10.0 ** (2.0 * r) - 1.0
+        x = 10.0 ** (3.0 * r - 1.0)
     elif k == "c5":
         v = rng.choice(np.array([1.0, 0.5, 2.5, 5.0]), count)
         a = _logu(rng, 0.5, 20.0, count)
