@@ -150,6 +150,26 @@ BLK_API blk_status blk_debug_split_f64(const double *v, const double *x, size_t 
                                        int nbins, void *scratch, int phases,
                                        cudaStream_t stream);
 
+/*
+ * Normal-inverse-Gaussian log-likelihood of a sample and its gradient, the
+ * application the paper motivates:
+ *   out[0] = sum_i log p(y_i),  out[1..4] = d/d(alpha, beta, delta, mu) of it,
+ *   log p(y) = log alpha + log delta - log pi + delta*gamma + beta*(y-mu)
+ *              - log q + log K_1(alpha*q),  q = sqrt(delta^2+(y-mu)^2),
+ *              gamma = sqrt(alpha^2 - beta^2),
+ * with log K_1 and dlogK_1/dz from the same plan + fixed-bin quadrature (v=1).
+ * y: DEVICE, n doubles.  out: DEVICE, 5 doubles (written, not accumulated).
+ * workspace: DEVICE, >= bessel_nig_workspace_bytes(n) bytes, caller-owned.
+ * Two kernels on `stream`; the block partials are reduced in a fixed order,
+ * so the result is bit-reproducible.  BLK_EINVAL unless |beta| < alpha,
+ * delta > 0 and all parameters finite.  n == 0 writes zeros.
+ */
+BLK_API size_t bessel_nig_workspace_bytes(size_t n);
+BLK_API blk_status bessel_nig_loglik_f64(const double *y, size_t n, double alpha,
+                                         double beta, double delta, double mu, int nbins,
+                                         double *out, void *workspace,
+                                         size_t workspace_bytes, cudaStream_t stream);
+
 /* Human-readable message for the last non-OK status on this thread. */
 BLK_API const char *bessel_logk_last_error(void);
 

@@ -23,7 +23,7 @@ __all__ = [
     "BLK_KERNEL_AUTO", "BLK_KERNEL_SIMPLE", "BLK_KERNEL_WS",
     "BesselLogKError", "lib", "library_path", "header_functions",
     "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
-    "host_workspace_bytes", "microbench", "DEFAULT_NBINS",
+    "host_workspace_bytes", "microbench", "DEFAULT_NBINS", "nig_loglik",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -78,6 +78,11 @@ def lib():
         L.bessel_logk_f64_host.argtypes = [vp, vp, sz, vp, vp, vp, ci, vp, sz, sz, vp]
         L.bessel_logk_last_error.restype = ctypes.c_char_p
         L.bessel_logk_version.restype = ctypes.c_char_p
+        L.bessel_nig_workspace_bytes.restype = sz
+        L.bessel_nig_workspace_bytes.argtypes = [sz]
+        cd = ctypes.c_double
+        L.bessel_nig_loglik_f64.restype = ci
+        L.bessel_nig_loglik_f64.argtypes = [vp, sz, cd, cd, cd, cd, ci, vp, vp, sz, vp]
         for name in ("blk_microbench_fp64", "blk_microbench_fp32", "blk_microbench_mufu"):
             f = getattr(L, name)
             f.restype = ci
@@ -205,3 +210,23 @@ def microbench(kind, blocks, threads, iters, out, stream=None):
     _check(f(int(blocks), int(threads), int(iters), ctypes.c_void_p(out.data_ptr()),
              _stream_handle(stream)))
     return blocks * threads * iters * BLK_MB_UNROLL
+
+
+def nig_loglik(y, alpha, beta, delta, mu, nbins=DEFAULT_NBINS, out=None, workspace=None,
+               stream=None):
+    """Sum of NIG log-densities of the float64 CUDA tensor ``y`` and its gradient in
+    (alpha, beta, delta, mu): returns a CUDA float64 tensor of 5 values (one device pass,
+    no host sync).  See include/bessel_logk.h (bessel_nig_loglik_f64)."""
+    import torch
+    n = y.numel()
+    py = _dev_ptr(y, torch.float64, n, "y")
+    if out is None:
+        out = torch.empty(5, dtype=torch.float64, device=y.device)
+    nbytes = lib().bessel_nig_workspace_bytes(n)
+    if workspace is None or workspace.numel() * workspace.element_size() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=y.device)
+    _check(lib().bessel_nig_loglik_f64(
+        py, n, float(alpha), float(beta), float(delta), float(mu), int(nbins),
+        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+        workspace.numel() * workspace.element_size(), _stream_handle(stream)))
+    return out

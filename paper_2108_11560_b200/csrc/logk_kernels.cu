@@ -20,6 +20,7 @@
 #include "logk_range.cuh"
 #include "logk_ws.cuh"
 #include "logk_split.cuh"
+#include "logk_nig.cuh"
 
 namespace blk {
 
@@ -461,6 +462,34 @@ blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, doub
   cudaEventDestroy(start_ev);
   if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "synchronize");
   return BLK_OK;
+}
+
+size_t bessel_nig_workspace_bytes(size_t n) {
+  const size_t blocks = (n + blk::kNigThreads - 1) / blk::kNigThreads;
+  return (blocks > 0 ? blocks : 1) * blk::kNigOut * sizeof(double);
+}
+
+blk_status bessel_nig_loglik_f64(const double *y, size_t n, double alpha, double beta,
+                                 double delta, double mu, int nbins, double *out,
+                                 void *workspace, size_t workspace_bytes, cudaStream_t s) {
+  if (nbins < 2 || nbins > BLK_MAX_NBINS) return fail(BLK_EINVAL, "nbins out of range [2, 65536]");
+  if (!out) return fail(BLK_EINVAL, "out is NULL");
+  if (!(alpha > fabs(beta)) || !(delta > 0.0) || !isfinite(alpha) || !isfinite(delta) ||
+      !isfinite(mu) || !isfinite(beta))
+    return fail(BLK_EINVAL, "NIG parameters need |beta| < alpha, delta > 0, all finite");
+  if (n > 0 && !y) return fail(BLK_EINVAL, "y is NULL");
+  if (!workspace || workspace_bytes < bessel_nig_workspace_bytes(n))
+    return fail(BLK_EINVAL, "workspace missing or too small");
+  const size_t blocks = (n + blk::kNigThreads - 1) / blk::kNigThreads;
+  if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "n too large");
+  const double gamma = sqrt(alpha * alpha - beta * beta);
+  double *partial = (double *)workspace;
+  if (blocks > 0)
+    blk::nig_f64_kernel<<<(unsigned)blocks, blk::kNigThreads, 0, s>>>(y, n, alpha, beta, delta, mu,
+                                                                     gamma, nbins, partial);
+  blk::nig_final_kernel<<<1, 256, 0, s>>>(partial, blocks, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "nig kernels");
 }
 
 blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, double *logk,

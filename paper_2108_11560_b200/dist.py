@@ -32,6 +32,22 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def allreduce_sum(t):
+    """Sum a small tensor (e.g. the 5 NIG log-likelihood sums) over all ranks in
+    place -- the one collective of the NIG path (NCCL over NVLink on B200)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t
+
+
+def nig_loglik_sharded(y_local, alpha, beta, delta, mu, nbins=128):
+    """Per-rank NIG sums on this rank's shard (CUDA kernels), then all_reduce."""
+    import paper_2108_11560_b200 as blk
+    out = blk.nig_loglik(y_local, alpha, beta, delta, mu, nbins=nbins)
+    return allreduce_sum(out)
+
+
 def gather_samples(local: dict, lo: int, hi: int, global_idx, device=None) -> dict:
     """local: kind -> 1-D tensor holding this rank's shard [lo, hi).
     Returns kind -> tensor of len(global_idx) (identical on every rank)."""
