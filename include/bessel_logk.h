@@ -151,6 +151,25 @@ BLK_API blk_status blk_debug_split_f64(const double *v, const double *x, size_t 
                                        cudaStream_t stream);
 
 /*
+ * Second derivatives in the same pass: from the
+ * second-order differentiated integrands of Sec. 4.1 (f^{(n,m)},
+ * n+m = 2) over f's range and nodes,
+ *   d2_dv2  = d^2 log K / dv^2   = S11/S0 - (S1/S0)^2,   S11 = sum w t^2
+ *   d2_dx2  = d^2 log K / dx^2   = S22/S0 - (S2/S0)^2,   S22 = sum w cosh^2 t
+ *   d2_dvdx = d^2 log K / dv dx  = S1 S2/S0^2 - S12/S0,   S12 = sum w t tanh(vt) cosh t
+ * plus log K, dlogK/dv, dlogK/dx as bessel_logk_f64.  All pointers DEVICE,
+ * n doubles each, any may be NULL (at least one not).  d2_dvdx is odd in v.
+ * The differences of moments lose |S11/S0|/|d2_dv2| (and alike) in relative
+ * precision -- the conditioning of the quantities themselves.  Options as for
+ * bessel_logk_f64_ex (the WS kernel variant is not available).
+ */
+BLK_API blk_status bessel_logk_hess_f64(const double *v, const double *x, size_t n,
+                                        double *logk, double *dlogk_dv, double *dlogk_dx,
+                                        double *d2_dv2, double *d2_dx2, double *d2_dvdx,
+                                        int nbins, const blk_options *opts,
+                                        cudaStream_t stream);
+
+/*
  * Normal-inverse-Gaussian log-likelihood of a sample and its gradient, the
  * application the paper motivates:
  *   out[0] = sum_i log p(y_i),  out[1..4] = d/d(alpha, beta, delta, mu) of it,

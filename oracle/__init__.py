@@ -55,6 +55,11 @@ def _load():
             lib.oracle_logk_literal_cm.restype = ctypes.c_int
             lib.oracle_logk_literal_cm.argtypes = [dp, dp, ctypes.c_size_t, dp,
                                                    ctypes.c_int, ctypes.c_double]
+            lib.oracle_logk_hess.restype = ctypes.c_int
+            lib.oracle_logk_hess.argtypes = [dp, dp, ctypes.c_size_t, dp, dp, dp, dp,
+                                             ctypes.c_int, ctypes.c_double]
+            lib.brute_logk_hess.restype = ctypes.c_int
+            lib.brute_logk_hess.argtypes = [dp, dp, ctypes.c_size_t, dp, ctypes.c_int]
             lib.brute_logk.restype = ctypes.c_int
             lib.brute_logk.argtypes = [dp, dp, ctypes.c_size_t, dp, dp, dp,
                                        ctypes.c_int]
@@ -173,3 +178,50 @@ def g1(v, x, t):
 
 def g2(v, x, t):
     return _load().oracle_g2(float(v), float(x), float(t))
+
+
+def logk_hess(v, x, nbins: int = 128, threads: int = 1):
+    """Oracle second derivatives: (log K, dv, dx, dvv, dxx, dvx) as float64 arrays."""
+    lib = _load()
+    v = _as_f64(v).ravel()
+    x = _as_f64(x).ravel()
+    n = v.size
+    lk, dv, dx = np.empty(n), np.empty(n), np.empty(n)
+    hs = np.empty((n, 3))
+
+    def run(lo, hi):
+        if hi > lo:
+            lib.oracle_logk_hess(v.ctypes.data + 8 * lo, x.ctypes.data + 8 * lo, hi - lo,
+                                 lk.ctypes.data + 8 * lo, dv.ctypes.data + 8 * lo,
+                                 dx.ctypes.data + 8 * lo, hs.ctypes.data + 24 * lo,
+                                 int(nbins), log_eps_f64())
+
+    if threads <= 1 or n < 1024:
+        run(0, n)
+    else:
+        bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda k: run(int(bounds[k]), int(bounds[k + 1])), range(threads)))
+    return lk, dv, dx, hs[:, 0].copy(), hs[:, 1].copy(), hs[:, 2].copy()
+
+
+def brute_hess(v, x, nbins: int = 1 << 14, threads: int = 1):
+    """Plain-definition long-double second derivatives (dvv, dxx, dvx)."""
+    lib = _load()
+    v = _as_f64(v).ravel()
+    x = _as_f64(x).ravel()
+    n = v.size
+    hs = np.empty((n, 3))
+
+    def run(lo, hi):
+        if hi > lo:
+            lib.brute_logk_hess(v.ctypes.data + 8 * lo, x.ctypes.data + 8 * lo, hi - lo,
+                                hs.ctypes.data + 24 * lo, int(nbins))
+
+    if threads <= 1:
+        run(0, n)
+    else:
+        bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda k: run(int(bounds[k]), int(bounds[k + 1])), range(threads)))
+    return hs[:, 0].copy(), hs[:, 1].copy(), hs[:, 2].copy()

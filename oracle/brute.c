@@ -42,8 +42,26 @@ static ld b_d2logf(ld v, ld x, ld t)
  * Returns 0 or -1 on bad arguments.  Elements with x <= 0 / non-finite
  * inputs get NaN.
  */
+static int brute_core(const double *v_in, const double *x_in, size_t n,
+                      double *logk, double *dlogk_dv, double *dlogk_dx, double *hess,
+                      int nbins);
+
 int brute_logk(const double *v_in, const double *x_in, size_t n,
                double *logk, double *dlogk_dv, double *dlogk_dx, int nbins)
+{
+    return brute_core(v_in, x_in, n, logk, dlogk_dv, dlogk_dx, NULL, nbins);
+}
+
+/* Second derivatives of log K (d2/dv2, d2/dx2, d2/dvdx; 3 per element) from
+ * the second-order differentiated integrands, plain definition. */
+int brute_logk_hess(const double *v_in, const double *x_in, size_t n, double *hess, int nbins)
+{
+    return brute_core(v_in, x_in, n, NULL, NULL, NULL, hess, nbins);
+}
+
+static int brute_core(const double *v_in, const double *x_in, size_t n,
+                      double *logk, double *dlogk_dv, double *dlogk_dx, double *hess,
+                      int nbins)
 {
     if (nbins < 2)
         return -1;
@@ -53,6 +71,7 @@ int brute_logk(const double *v_in, const double *x_in, size_t n,
             if (logk) logk[i] = NAN;
             if (dlogk_dv) dlogk_dv[i] = NAN;
             if (dlogk_dx) dlogk_dx[i] = NAN;
+            if (hess) hess[3 * i] = hess[3 * i + 1] = hess[3 * i + 2] = NAN;
             continue;
         }
         ld sgn = vs < 0 ? -1.0L : 1.0L;
@@ -81,18 +100,28 @@ int brute_logk(const double *v_in, const double *x_in, size_t n,
         while (b_logf(v, x, tb) > gp - 60.0L)
             tb += step;
         ld h = (tb - ta) / nbins;
-        ld S0 = 0, S1 = 0, S2 = 0;
+        ld S0 = 0, S1 = 0, S2 = 0, S11 = 0, S22 = 0, S12 = 0;
         for (int m = 0; m <= nbins; ++m) {
             ld t = ta + m * h;
             ld c = (m == 0 || m == nbins) ? 0.5L : 1.0L;
             ld w = c * expl(b_logf(v, x, t) - gp);
+            ld ch = coshl(t), th = tanhl(v * t);
             S0 += w;
-            S1 += w * t * tanhl(v * t);
-            S2 += w * coshl(t);
+            S1 += w * t * th;
+            S2 += w * ch;
+            S11 += w * t * t;
+            S22 += w * ch * ch;
+            S12 += w * t * th * ch;
         }
         if (logk) logk[i] = (double)(gp + logl(h) + logl(S0));
         if (dlogk_dv) dlogk_dv[i] = (double)(sgn * S1 / S0);
         if (dlogk_dx) dlogk_dx[i] = (double)(-S2 / S0);
+        if (hess) {
+            ld m1 = S1 / S0, m2 = S2 / S0;
+            hess[3 * i] = (double)(S11 / S0 - m1 * m1);
+            hess[3 * i + 1] = (double)(S22 / S0 - m2 * m2);
+            hess[3 * i + 2] = (double)(sgn * (-S12 / S0 + m1 * m2));
+        }
     }
     return 0;
 }

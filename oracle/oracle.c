@@ -168,12 +168,35 @@ static int oracle_plan(oracle_ctx *c, int max_iter, double tol,
  * accumulated over f's own range and nodes (R14).
  *   log K = g_p + log h + log S0,  dlogK/dv = sign(v) S1/S0,  dlogK/dx = -S2/S0
  */
+static void oracle_one_h(double v_in, double x, int nbins, int max_iter, double tol,
+                         double log_eps, double *logk, double *dv, double *dx,
+                         double *plan, double *hess);
+
 static void oracle_one(double v_in, double x, int nbins, int max_iter, double tol,
                        double log_eps, double *logk, double *dv, double *dx,
                        double *plan)
 {
+    oracle_one_h(v_in, x, nbins, max_iter, tol, log_eps, logk, dv, dx, plan, NULL);
+}
+
+/*
+ * Same, plus (when hess != NULL) the second derivatives from the second-order
+ * differentiated integrands of Sec. 4.1 (f^{(n,m)} with n+m = 2),
+ * accumulated over f's range and nodes like the first-order ones (R14):
+ *   d2K/dv2   = int t^2 cosh(vt) e^{-x cosh t}          -> S11 = sum w t^2
+ *   d2K/dx2   = int cosh^2 t cosh(vt) e^{-x cosh t}     -> S22 = sum w cosh^2 t
+ *   d2K/dvdx  = -int t cosh t sinh(vt) e^{-x cosh t}    -> S12 = sum w t tanh(vt) cosh t
+ *   hess[0] = d2logK/dv2  = S11/S0 - (S1/S0)^2
+ *   hess[1] = d2logK/dx2  = S22/S0 - (S2/S0)^2
+ *   hess[2] = d2logK/dvdx = -S12/S0 + (S1/S0)(S2/S0)     (odd in v, like dv)
+ */
+static void oracle_one_h(double v_in, double x, int nbins, int max_iter, double tol,
+                         double log_eps, double *logk, double *dv, double *dx,
+                         double *plan, double *hess)
+{
     double nanv = NAN;
     if (plan) { plan[0] = plan[1] = plan[2] = plan[3] = nanv; }
+    if (hess) { hess[0] = hess[1] = hess[2] = nanv; }
     if (!(x > 0.0) || !isfinite(x) || !isfinite(v_in)) { /* R16 */
         *logk = *dv = *dx = nanv;
         return;
@@ -187,7 +210,7 @@ static void oracle_one(double v_in, double x, int nbins, int max_iter, double to
     }
     if (plan) { plan[0] = tp; plan[1] = c.gp; plan[2] = t0; plan[3] = t1; }
     double h = (t1 - t0) / nbins;                        /* P:228 */
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0;
     for (int m = 0; m <= nbins; ++m) {
         double t = t0 + m * h;                           /* P:228 */
         double cm = (m == 0 || m == nbins) ? 0.5 : 1.0;  /* P:231 */
@@ -195,10 +218,18 @@ static void oracle_one(double v_in, double x, int nbins, int max_iter, double to
         S0 += w;
         S1 += w * t * tanh(c.v * t);
         S2 += w * cosh(t);
+        S11 += w * t * t;
+        S22 += w * cosh(t) * cosh(t);
+        S12 += w * t * tanh(c.v * t) * cosh(t);
     }
     *logk = c.gp + log(h) + log(S0);                     /* P:236 */
     *dv = s * S1 / S0;
     *dx = -S2 / S0;
+    if (hess) {
+        hess[0] = S11 / S0 - (S1 / S0) * (S1 / S0);
+        hess[1] = S22 / S0 - (S2 / S0) * (S2 / S0);
+        hess[2] = s * (-S12 / S0 + (S1 / S0) * (S2 / S0));
+    }
 }
 
 /* ---------------- exported (C ABI, loaded by tests via ctypes) ------------- */
@@ -227,6 +258,26 @@ int oracle_logk(const double *v, const double *x, size_t n,
         double a, b, d;
         oracle_one(v[i], x[i], nbins, max_iter, tol, log_eps, &a, &b, &d,
                    plan ? plan + 4 * i : NULL);
+        if (logk) logk[i] = a;
+        if (dlogk_dv) dlogk_dv[i] = b;
+        if (dlogk_dx) dlogk_dx[i] = d;
+    }
+    return 0;
+}
+
+/*
+ * Second derivatives (see oracle_one_h): hess has 3 doubles per element
+ * (d2/dv2, d2/dx2, d2/dvdx); logk/dv/dx as in oracle_logk (may be NULL).
+ */
+int oracle_logk_hess(const double *v, const double *x, size_t n,
+                     double *logk, double *dlogk_dv, double *dlogk_dx, double *hess,
+                     int nbins, double log_eps)
+{
+    if (nbins < 1 || !hess)
+        return -1;
+    for (size_t i = 0; i < n; ++i) {
+        double a, b, d;
+        oracle_one_h(v[i], x[i], nbins, 10, 0.0, log_eps, &a, &b, &d, NULL, hess + 3 * i);
         if (logk) logk[i] = a;
         if (dlogk_dv) dlogk_dv[i] = b;
         if (dlogk_dx) dlogk_dx[i] = d;

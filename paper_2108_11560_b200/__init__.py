@@ -23,7 +23,7 @@ __all__ = [
     "BLK_KERNEL_AUTO", "BLK_KERNEL_SIMPLE", "BLK_KERNEL_WS",
     "BesselLogKError", "lib", "library_path", "header_functions",
     "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
-    "host_workspace_bytes", "microbench", "DEFAULT_NBINS", "nig_loglik",
+    "host_workspace_bytes", "microbench", "DEFAULT_NBINS", "nig_loglik", "log_bessel_k_hess",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -78,6 +78,9 @@ def lib():
         L.bessel_logk_f64_host.argtypes = [vp, vp, sz, vp, vp, vp, ci, vp, sz, sz, vp]
         L.bessel_logk_last_error.restype = ctypes.c_char_p
         L.bessel_logk_version.restype = ctypes.c_char_p
+        L.bessel_logk_hess_f64.restype = ci
+        L.bessel_logk_hess_f64.argtypes = [vp, vp, sz, vp, vp, vp, vp, vp, vp, ci,
+                                           ctypes.POINTER(_Options), vp]
         L.bessel_nig_workspace_bytes.restype = sz
         L.bessel_nig_workspace_bytes.argtypes = [sz]
         cd = ctypes.c_double
@@ -230,3 +233,17 @@ def nig_loglik(y, alpha, beta, delta, mu, nbins=DEFAULT_NBINS, out=None, workspa
         ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
         workspace.numel() * workspace.element_size(), _stream_handle(stream)))
     return out
+
+
+def log_bessel_k_hess(v, x, nbins=DEFAULT_NBINS, stream=None, lanes_per_element=0,
+                      range_mode=BLK_RANGE_AUTO):
+    """(log K, dv, dx, d2/dv2, d2/dx2, d2/dvdx) of float64 CUDA tensors in one pass."""
+    import torch
+    n = v.numel()
+    pv = _dev_ptr(v, torch.float64, n, "v")
+    px = _dev_ptr(x, torch.float64, n, "x")
+    outs = [torch.empty_like(v) for _ in range(6)]
+    o = _Options(int(lanes_per_element), int(range_mode), 0, 0)
+    _check(lib().bessel_logk_hess_f64(pv, px, n, *[ctypes.c_void_p(t.data_ptr()) for t in outs],
+                                      int(nbins), ctypes.byref(o), _stream_handle(stream)))
+    return tuple(outs)

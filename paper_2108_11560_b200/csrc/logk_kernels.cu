@@ -99,6 +99,63 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   if (DX) dlogk_dx[i] = ok ? -(s.S2 * r) : nanv;
 }
 
+// Second derivatives in the same pass: the three
+// second-order sums of Sec. 4.1 over f's range and nodes.  Outputs may each
+// be NULL; all six sums are always formed.
+template <int LPE>
+__global__ void __launch_bounds__(128, BLK_MINB)
+logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
+                     double *__restrict__ logk, double *__restrict__ dv_out,
+                     double *__restrict__ dx_out, double *__restrict__ dvv_out,
+                     double *__restrict__ dxx_out, double *__restrict__ dvx_out, int nbins,
+                     int range_mode) {
+  load_exp_table();
+  __syncthreads();
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = gtid / LPE;
+  const int sub = (int)(gtid % LPE);
+  const bool live = i < n_el;
+  const double vraw = live ? vin[i] : 1.0;
+  const double x = live ? xin[i] : 1.0;
+  const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
+  const double v = fabs(vraw);
+  const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
+  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
+  bool ok = false;
+  if (valid) {
+    if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
+      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64);
+      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
+    } else {
+      const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
+      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
+    }
+    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+  }
+  Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const double h = (t1 - t0) * rcp64((double)nbins);
+  if (ok) {
+    int mb, me;
+    lane_bins<LPE>(nbins, sub, mb, me);
+    if (dmin > -600.0) s = quad_f64<true, true, false, true>(v, x, t0, h, gp, nbins, mb, me, g_exp_tab);
+    else s = quad_f64<true, true, true, true>(v, x, t0, h, gp, nbins, mb, me, g_exp_tab);
+  }
+  if (LPE > 1) {
+    s.S0 = group_sum<LPE>(s.S0); s.S1 = group_sum<LPE>(s.S1); s.S2 = group_sum<LPE>(s.S2);
+    s.S11 = group_sum<LPE>(s.S11); s.S22 = group_sum<LPE>(s.S22); s.S12 = group_sum<LPE>(s.S12);
+  }
+  if (!live || sub != 0) return;
+  const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
+  const double r = rcp64(s.S0);
+  const double m1 = s.S1 * r, m2 = s.S2 * r;
+  if (logk) logk[i] = ok ? gp + log(h * s.S0) : nanv;
+  if (dv_out) dv_out[i] = ok ? sgn * m1 : nanv;
+  if (dx_out) dx_out[i] = ok ? -m2 : nanv;
+  if (dvv_out) dvv_out[i] = ok ? fma(-m1, m1, s.S11 * r) : nanv;
+  if (dxx_out) dxx_out[i] = ok ? fma(-m2, m2, s.S22 * r) : nanv;
+  if (dvx_out) dvx_out[i] = ok ? sgn * fma(m1, m2, -(s.S12 * r)) : nanv;
+}
+
 template <bool LOGK, bool DV, bool DX, int LPE>
 __global__ void __launch_bounds__(128)
 logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, size_t n_el,
@@ -490,6 +547,36 @@ blk_status bessel_nig_loglik_f64(const double *y, size_t n, double alpha, double
   blk::nig_final_kernel<<<1, 256, 0, s>>>(partial, blocks, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BLK_OK : cuda_fail(e, "nig kernels");
+}
+
+blk_status bessel_logk_hess_f64(const double *v, const double *x, size_t n, double *logk,
+                                double *dlogk_dv, double *dlogk_dx, double *d2_dv2,
+                                double *d2_dx2, double *d2_dvdx, int nbins,
+                                const blk_options *opts, cudaStream_t stream) {
+  int lanes, mode, th, kernel;
+  const bool any = logk || dlogk_dv || dlogk_dx || d2_dv2 || d2_dx2 || d2_dvdx;
+  blk_status st = validate(v, x, n, any ? (void *)1 : nullptr, nullptr, nullptr, nbins, opts,
+                           lanes, mode, th, kernel);
+  if (st != BLK_OK) return st;
+  if (kernel == BLK_KERNEL_WS) return fail(BLK_EINVAL, "no warp-specialized Hessian kernel");
+  if (n == 0) return BLK_OK;
+  const size_t total = n * (size_t)lanes;
+  const size_t blocks = (total + th - 1) / th;
+  if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "grid too large");
+#define BLK_HESS_LAUNCH(L)                                                                    \
+  blk::logk_f64_hess_kernel<L><<<(unsigned)blocks, th, 0, stream>>>(                          \
+      v, x, n, logk, dlogk_dv, dlogk_dx, d2_dv2, d2_dx2, d2_dvdx, nbins, mode)
+  switch (lanes) {
+    case 1: BLK_HESS_LAUNCH(1); break;
+    case 2: BLK_HESS_LAUNCH(2); break;
+    case 4: BLK_HESS_LAUNCH(4); break;
+    case 8: BLK_HESS_LAUNCH(8); break;
+    case 16: BLK_HESS_LAUNCH(16); break;
+    default: BLK_HESS_LAUNCH(32); break;
+  }
+#undef BLK_HESS_LAUNCH
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "hess kernel launch");
 }
 
 blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, double *logk,

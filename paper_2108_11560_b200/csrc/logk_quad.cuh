@@ -40,22 +40,10 @@ constexpr int kAnchor = BLK_ANCHOR; // FP64 re-anchoring interval for e^{+-t} (n
 #ifndef BLK_GROUP
 #define BLK_GROUP 4
 #endif
-#ifndef BLK_ACC2
-#define BLK_ACC2 0
-#endif
 #ifndef BLK_MINB
 #define BLK_MINB 6
 #endif
 constexpr int kGroup = BLK_GROUP; // nodes evaluated together (independent exp chains)
-constexpr bool kAcc2 = BLK_ACC2;  // split the sums over two accumulator sets
-#ifndef BLK_LOCKSTEP
-#define BLK_LOCKSTEP 1
-#endif
-constexpr bool kLockstep = BLK_LOCKSTEP;  // stage-by-stage evaluation of a group
-#ifndef BLK_I2F
-#define BLK_I2F 0
-#endif
-constexpr bool kI2F = BLK_I2F;    // k as double by I2F.F64 instead of kd - magic
 
 __device__ __align__(16) const double kExp2Table[kExpTab] = {
 #include "exp2_table.inc"
@@ -155,45 +143,63 @@ __device__ __forceinline__ double one_minus_exp(double z, const double *__restri
 }
 
 struct Sums64 {
-  double S0, S1, S2;
+  double S0, S1, S2;        // sum w, sum E t p, sum w cosh t      (Sec. 4.1, first order)
+  double S11, S22, S12;     // sum w t^2, sum w cosh^2 t, sum E t p cosh t (second order)
 };
 
-// One node's contributions, given cosh t, q = e^{-2vt} and p = 1 - q.
-template <bool DV, bool DX, bool CLAMP>
+// Accumulates one node: E = exp(vt - x cosh t - s - log 2), q = e^{-2vt},
+// p = 1 - q, so w = E (1 + q) = e^{g(t) - s} and E t p = t tanh(vt) e^{g - s}.
+template <bool DV, bool DX, bool HESS>
+__device__ __forceinline__ void accumulate(Sums64 &s, double E, double q, double p, double t,
+                                           double ch) {
+  const double w = fma(E, q, E);
+  s.S0 += w;
+  if (HESS) {
+    const double wc = w * ch, wt = w * t, etp = (E * t) * p;
+    s.S2 += wc;
+    s.S22 = fma(wc, ch, s.S22);
+    s.S11 = fma(wt, t, s.S11);
+    s.S1 += etp;
+    s.S12 = fma(etp, ch, s.S12);
+  } else {
+    if (DX) s.S2 = fma(w, ch, s.S2);
+    if (DV) s.S1 = fma(E * t, p, s.S1);
+  }
+}
+
+// One node's contributions, given cosh t, q and p.
+template <bool DV, bool DX, bool HESS, bool CLAMP>
 __device__ __forceinline__ void node_acc(double v, double x, double s_mid, double t, double ch,
                                          double q, double p, const double *__restrict__ tab,
-                                         double &S0, double &S1, double &S2) {
-  const double E = exp_tab<CLAMP>(fma(-x, ch, fma(v, t, -s_mid)), tab);
-  const double w = fma(E, q, E);                     // E (1 + q)
-  S0 += w;
-  if (DX) S2 = fma(w, ch, S2);
-  if (DV) S1 = fma(E * t, p, S1);
+                                         Sums64 &s) {
+  accumulate<DV, DX, HESS>(s, exp_tab<CLAMP>(fma(-x, ch, fma(v, t, -s_mid)), tab), q, p, t, ch);
 }
 
 // Nodes [ib, ie) with weight 1.  Node positions are t0 + m h to 1 ulp (an
 // accumulated t += h would drift by m ulp, which v t amplifies for large v);
 // e^{+-t} are re-anchored every kAnchor nodes, q and p advance across chunks.
-template <bool DV, bool DX, bool CLAMP>
+// Nodes go in groups of kGroup whose exponentials are evaluated stage by
+// stage (independent dependency chains interleaved).
+template <bool DV, bool DX, bool HESS, bool CLAMP>
 __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double h,
                                            double s_mid, int ib, int ie,
-                                           const double *__restrict__ tab, Sums64 &s) {
+                                           const double *__restrict__ tab, Sums64 &out) {
   if (ie <= ib) return;
+  constexpr bool NEEDP = DV || HESS;
   const double m2v = -2.0 * v;
   const double eh = exp_tab<false>(h, tab);
   const double ehi = rcp64(eh);
   const double tb = fma((double)ib, h, t0);
   double q = exp_tab<true>(m2v * tb, tab);           // q_m = e^{-2 v t_m}
   const double eq = exp_tab<true>(m2v * h, tab);
-  double p = DV ? one_minus_exp(m2v * tb, tab) : 0.0;  // p_m = 1 - q_m
-  const double a1 = DV ? one_minus_exp(m2v * h, tab) : 0.0;
-  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
-  double T0 = 0.0, T1 = 0.0, T2 = 0.0;               // second accumulator set (kAcc2)
+  double p = NEEDP ? one_minus_exp(m2v * tb, tab) : 0.0;  // p_m = 1 - q_m
+  const double a1 = NEEDP ? one_minus_exp(m2v * h, tab) : 0.0;
+  Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   // chunks of kAnchor nodes (a multiple of kGroup), the last one shorter
-  constexpr int csz = kAnchor;
   static_assert(kAnchor % kGroup == 0, "anchor interval must hold whole groups");
 #pragma unroll 1
-  for (int c0 = ib; c0 < ie; c0 += csz) {
-    const int c1 = min(c0 + csz, ie);
+  for (int c0 = ib; c0 < ie; c0 += kAnchor) {
+    const int c1 = min(c0 + kAnchor, ie);
     double tc = fma((double)c0, h, t0);
     double et = 0.5 * exp_tab<true>(fmin(tc, 709.0), tab);   // e^t / 2
     double eti = 0.25 * rcp64(et);                           // e^-t / 2
@@ -201,9 +207,10 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
       // node 0 has weight 1/2: take half of it back.  It is exact
       // here (anchored state) and may be the largest node (t0 = 0 when the
       // peak region reaches t = 0), so this correction is done in FP64.
-      double h0 = 0.0, h1 = 0.0, h2 = 0.0;
-      node_acc<DV, DX, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, h0, h1, h2);
-      S0 -= 0.5 * h0; S1 -= 0.5 * h1; S2 -= 0.5 * h2;
+      Sums64 z{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      node_acc<DV, DX, HESS, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, z);
+      s.S0 -= 0.5 * z.S0; s.S1 -= 0.5 * z.S1; s.S2 -= 0.5 * z.S2;
+      s.S11 -= 0.5 * z.S11; s.S22 -= 0.5 * z.S22; s.S12 -= 0.5 * z.S12;
     }
     int m = c0;
 #pragma unroll 1
@@ -217,85 +224,61 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
         eti *= ehi;
         qg[j] = q;
         pg[j] = p;
-        if (DV) p = fma(q, a1, p);
+        if (NEEDP) p = fma(q, a1, p);
         q *= eq;
       }
-      if (kLockstep) {
-        // the group's exponentials stage by stage, so consecutive dependent
-        // FP64 instructions of one node are kGroup instructions apart
-        double a[kGroup], kd[kGroup], r[kGroup], pp[kGroup], E[kGroup];
-        int k[kGroup];
+      // the group's exponentials stage by stage, so consecutive dependent
+      // FP64 instructions of one node are kGroup instructions apart
+      double a[kGroup], kd[kGroup], r[kGroup], pp[kGroup], tj[kGroup];
+      int k[kGroup];
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) a[j] = fma(v, tg[j], -s_mid);
+      for (int j = 0; j < kGroup; ++j) a[j] = fma(v, tg[j], -s_mid);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          a[j] = fma(-x, chg[j], a[j]);
-          if (CLAMP) a[j] = a[j] < -707.0 ? -707.0 : a[j];
-        }
+      for (int j = 0; j < kGroup; ++j) {
+        a[j] = fma(-x, chg[j], a[j]);
+        if (CLAMP) a[j] = a[j] < -707.0 ? -707.0 : a[j];
+      }
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) kd[j] = fma(a[j], kExpInvL, kExpMagic);
+      for (int j = 0; j < kGroup; ++j) kd[j] = fma(a[j], kExpInvL, kExpMagic);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          k[j] = __double2loint(kd[j]);
-          kd[j] = kI2F ? __int2double_rn(k[j]) : kd[j] - kExpMagic;
-        }
-        double tj[kGroup];
+      for (int j = 0; j < kGroup; ++j) {
+        k[j] = __double2loint(kd[j]);
+        kd[j] -= kExpMagic;
+      }
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) tj[j] = exp_table_entry(k[j] & (kExpTab - 1));
+      for (int j = 0; j < kGroup; ++j) tj[j] = exp_table_entry(k[j] & (kExpTab - 1));
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
+      for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) pp[j] = fma(r[j], 1.6666666666666666e-01, 0.5);
+      for (int j = 0; j < kGroup; ++j) pp[j] = fma(r[j], 1.6666666666666666e-01, 0.5);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j] * r[j], r[j]);
+      for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j] * r[j], r[j]);
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          const double res = fma(tj[j], pp[j], tj[j]);
-          E[j] = __hiloint2double(add_exponent(__double2hiint(res), k[j] >> kExpBits),
-                                  __double2loint(res));
-        }
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          const double w = fma(E[j], qg[j], E[j]);
-          if (kAcc2 && (j & 1)) {
-            T0 += w;
-            if (DX) T2 = fma(w, chg[j], T2);
-            if (DV) T1 = fma(E[j] * tg[j], pg[j], T1);
-          } else {
-            S0 += w;
-            if (DX) S2 = fma(w, chg[j], S2);
-            if (DV) S1 = fma(E[j] * tg[j], pg[j], S1);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          if (kAcc2 && (j & 1))
-            node_acc<DV, DX, CLAMP>(v, x, s_mid, tg[j], chg[j], qg[j], pg[j], tab, T0, T1, T2);
-          else
-            node_acc<DV, DX, CLAMP>(v, x, s_mid, tg[j], chg[j], qg[j], pg[j], tab, S0, S1, S2);
-        }
+      for (int j = 0; j < kGroup; ++j) {
+        const double res = fma(tj[j], pp[j], tj[j]);
+        const double E = __hiloint2double(add_exponent(__double2hiint(res), k[j] >> kExpBits),
+                                          __double2loint(res));
+        accumulate<DV, DX, HESS>(s, E, qg[j], pg[j], tg[j], chg[j]);
       }
       tc = fma((double)(m + kGroup), h, t0);
     }
 #pragma unroll 1
     for (; m < c1; ++m) {                            // remainder
-      node_acc<DV, DX, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, S0, S1, S2);
-      if (DV) p = fma(q, a1, p);
+      node_acc<DV, DX, HESS, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, s);
+      if (NEEDP) p = fma(q, a1, p);
       q *= eq;
       et *= eh; eti *= ehi;
       tc = fma((double)(m + 1), h, t0);
     }
   }
-  s.S0 += S0 + T0;
-  s.S1 += S1 + T1;
-  s.S2 += S2 + T2;
+  out.S0 += s.S0; out.S1 += s.S1; out.S2 += s.S2;
+  out.S11 += s.S11; out.S22 += s.S22; out.S12 += s.S12;
 }
 
 // Half of the last node's contributions, evaluated in FP32: that node sits
 // below the eps level of the peak (d(t1) < 0), so its terms are < 2^-52 of
 // the sums and FP32 is exact to far below double rounding there.
-template <bool DV, bool DX>
+template <bool DV, bool DX, bool HESS>
 __device__ __forceinline__ void end_half_f32(double v, double x, double s_mid, double t,
                                              Sums64 &s) {
   const float kL2e = 1.4426950408889634f;
@@ -307,25 +290,31 @@ __device__ __forceinline__ void end_half_f32(double v, double x, double s_mid, d
   const float E = 0.5f * ex2_approx(arg * kL2e);
   const float w = fmaf(E, q, E);
   if (!(w > 0.0f)) return;          // underflowed (or e^t overflowed FP32): nothing to take back
+  const double etp = double(E * tf) * (-expm1f(-2.0f * vf * tf));
   s.S0 -= w;
-  if (DX) s.S2 -= double(w) * ch;
-  if (DV) s.S1 -= double(E * tf) * (-expm1f(-2.0f * vf * tf));
+  if (DX || HESS) s.S2 -= double(w) * ch;
+  if (DV || HESS) s.S1 -= etp;
+  if (HESS) {
+    s.S11 -= double(w) * tf * tf;
+    s.S22 -= double(w) * ch * ch;
+    s.S12 -= etp * ch;
+  }
 }
 
 // Nodes [mb, me) of the n-interval trapezoid on [t0, t0 + n h] (node m at
 // t0 + m h; nodes 0 and n carry weight 1/2: all nodes are summed
 // with weight 1 and half of each end node is taken back).  The lane owning
 // node 0 has mb == 0, the lane owning node n has me == n + 1.
-template <bool DV, bool DX, bool CLAMP>
+template <bool DV, bool DX, bool CLAMP, bool HESS = false>
 __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double h,
                                            double shift, int n, int mb, int me,
                                            const double *__restrict__ tab) {
-  Sums64 s{0.0, 0.0, 0.0};
+  Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double s_mid = shift + kLn2;                 // E = exp(vt - x cosh t - s_mid)
-  nodes_fp64<DV, DX, CLAMP>(v, x, t0, h, s_mid, mb, me, tab, s);
+  nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, tab, s);
   // node n: t_n = t1 lies outside the eps-support (d(t1) < 0, FindZero
   // returns the outer end, R1), so its term is < 2^-52 of the peak term
-  if (me == n + 1) end_half_f32<DV, DX>(v, x, s_mid, fma((double)n, h, t0), s);
+  if (me == n + 1) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
   return s;
 }
 

@@ -292,3 +292,32 @@ def test_paper_accuracy_grid():
             assert res[name][k]["cells_ge_4"] == 0, (name, k, res[name][k])
         assert res[name]["logk"]["mean"] < 1.0, res[name]
         assert res[name]["dx"]["mean"] < 1.0, res[name]
+
+
+# ------------------------------------------------ second derivatives (§8(f) 1)
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c5"])
+@pytest.mark.parametrize("lanes", [1, 4])
+def test_parity_hessian(cfg, lanes):
+    """d2/dv2, d2/dx2, d2/dvdx in the same pass vs the oracle.  The outputs are
+    differences of moments (S11/S0 - (S1/S0)^2 ...), so both sides lose
+    |moment|/|result| in relative precision; the bound is 1e-10 of the result
+    plus 1e-12 of the moment it is formed from (north_star's 1e-10 for the
+    first derivatives)."""
+    v, x = workloads.generate(cfg, 0, 6001)
+    v = v.astype(np.float64)
+    x = x.astype(np.float64)
+    dev = torch.device("cuda")
+    out = blk.log_bessel_k_hess(torch.from_numpy(v).to(dev), torch.from_numpy(x).to(dev),
+                                lanes_per_element=lanes)
+    torch.cuda.synchronize()
+    got = [o.cpu().numpy() for o in out]
+    lk, dv, dx, dvv, dxx, dvx = oracle.logk_hess(v, x, NB, threads=8)
+    assert_parity({"logk": got[0], "dv": got[1], "dx": got[2]},
+                  {"logk": lk, "dv": dv, "dx": dx}, "f64", f"hess {cfg}")
+    for g, r, mom in ((got[3], dvv, np.abs(dvv) + dv * dv), (got[4], dxx, np.abs(dxx) + dx * dx),
+                      (got[5], dvx, np.abs(dvx) + np.abs(dv * dx))):
+        bad = np.abs(g - r) > 1e-10 * np.abs(r) + 1e-12 * mom
+        assert not bad.any(), (np.nonzero(bad)[0][:5], g[bad][:3], r[bad][:3])
+    # the Bessel ODE on the GPU outputs directly
+    ode = 1 + v * v / (x * x) - got[2] / x - got[2] ** 2
+    assert np.all(np.abs(got[4] - ode) <= 1e-11 * (np.abs(ode) + got[2] ** 2 + v * v / (x * x) + 1))

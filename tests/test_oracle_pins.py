@@ -290,3 +290,71 @@ def test_invalid_inputs_give_nan():
     lk, dv, dx = oracle.logk(v, x)
     assert np.all(np.isnan(lk[:6])) and np.all(np.isnan(dv[:6])) and np.all(np.isnan(dx[:6]))
     assert np.isfinite(lk[6])
+
+
+# ------------------------------------------------ second derivatives (§8(f) 1)
+def test_hess_closed_forms_dxx():
+    """d2/dx2 log K: 1/(2x^2) at v=1/2 and 1/(2x^2) + (2x+1)/(x^2 (x+1)^2) at v=3/2
+    (differentiating the DLMF 10.39.2 closed forms)."""
+    x = XGRID
+    for v, ref in ((0.5, 1 / (2 * x * x)),
+                   (1.5, 1 / (2 * x * x) + (2 * x + 1) / (x * x * (x + 1) ** 2))):
+        _, _, dx, dvv, dxx, dvx = oracle.logk_hess(np.full_like(x, v), x)
+        # S22/S0 - (S2/S0)^2 cancels by (dx^2)/|dxx| (5e5 at x=1e3): the error
+        # bound is relative to the moment S22/S0 = dxx + dx^2
+        assert np.all(np.abs(dxx - ref) <= 1e-14 * (np.abs(ref) + dx * dx)), v
+
+
+def test_hess_bessel_ode():
+    """K_v solves x^2 K'' + x K' - (x^2 + v^2) K = 0, i.e. with L = log K:
+    L'' = 1 + v^2/x^2 - L'/x - L'^2 -- ties the S22 sum to the S2 sum."""
+    rng = np.random.default_rng(12)
+    v = rng.uniform(0.0, 80.0, 400)
+    x = 10 ** rng.uniform(-2, 2.5, 400)
+    lk, dv, dx, dvv, dxx, dvx = oracle.logk_hess(v, x)
+    ref = 1 + v * v / (x * x) - dx / x - dx * dx
+    # conditioning: the right side is a difference of terms ~ dx^2
+    assert np.all(np.abs(dxx - ref) <= 1e-12 * (np.abs(ref) + dx * dx + v * v / (x * x) + 1))
+
+
+def test_hess_symmetry_and_order_zero():
+    """d2/dv2 and d2/dx2 even in v, d2/dvdx odd; d2/dvdx = 0 at v = 0."""
+    rng = np.random.default_rng(13)
+    v = rng.uniform(0, 50, 200)
+    x = 10 ** rng.uniform(-2, 2, 200)
+    a = oracle.logk_hess(v, x)
+    b = oracle.logk_hess(-v, x)
+    assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+    assert np.array_equal(a[5], -b[5])
+    z = oracle.logk_hess(np.zeros(20), x[:20])
+    assert np.all(z[5] == 0.0)
+
+
+def test_hess_vs_mpmath():
+    """Second derivatives against mpmath numerical differentiation of besselk."""
+    pts = [(0.5, 1.0), (3.0, 2.0), (40.0, 5.0), (0.0, 0.5), (12.0, 0.3), (80.0, 200.0)]
+    v = np.array([p[0] for p in pts])
+    x = np.array([p[1] for p in pts])
+    _, dv, dx, dvv, dxx, dvx = oracle.logk_hess(v, x)
+    for i, (vi, xi) in enumerate(pts):
+        f = lambda s, y: mpmath.log(mpmath.besselk(s, y))
+        rvv = float(mpmath.diff(lambda s: f(s, xi), vi, 2))
+        rxx = float(mpmath.diff(lambda y: f(vi, y), xi, 2))
+        rvx = float(mpmath.diff(f, (vi, xi), (1, 1)))
+        k_vv = abs(dvv[i]) + dv[i] ** 2
+        k_xx = abs(dxx[i]) + dx[i] ** 2
+        k_vx = abs(dvx[i]) + abs(dv[i] * dx[i])
+        assert abs(dvv[i] - rvv) <= 1e-13 * k_vv + 1e-14, (vi, xi, dvv[i], rvv)
+        assert abs(dxx[i] - rxx) <= 1e-13 * k_xx + 1e-14, (vi, xi, dxx[i], rxx)
+        assert abs(dvx[i] - rvx) <= 1e-13 * k_vx + 1e-14, (vi, xi, dvx[i], rvx)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_hess_vs_brute_force(cfg):
+    idx = workloads.sample_indices(cfg, 150, seed=14)
+    v, x = workloads.gather(cfg, idx)
+    _, dv, dx, dvv, dxx, dvx = oracle.logk_hess(v, x)
+    bvv, bxx, bvx = oracle.brute_hess(v, x, threads=8)
+    assert np.all(np.abs(dvv - bvv) <= 1e-13 * (np.abs(bvv) + dv * dv) + 1e-15)
+    assert np.all(np.abs(dxx - bxx) <= 1e-13 * (np.abs(bxx) + dx * dx) + 1e-15)
+    assert np.all(np.abs(dvx - bvx) <= 1e-13 * (np.abs(bvx) + np.abs(dv * dx)) + 1e-15)
