@@ -23,20 +23,10 @@ namespace blk {
 
 constexpr int kExpBits = 11;
 constexpr int kExpTab = 1 << kExpBits;   // 2^(j/2048), j = 0..2047, in shared memory (16 KB)
-#ifndef BLK_TAB_REP
-#define BLK_TAB_REP 1
-#endif
-// The table can be stored kTabRep times, interleaved (entry j of copy c at
-// j*kTabRep + c), with lane L reading copy L % kTabRep: 16 copies make the
-// per-node LDS.64 bank-conflict-free.  Measured on B200 (profiles/r01_*):
-// no gain -- the kernel is issue-bound, not LDS-bound -- and the 32 KB table
-// fill costs more, so the default is a single copy.
-constexpr int kTabRep = BLK_TAB_REP;
-constexpr int kTabSize = kExpTab * kTabRep;
 #ifndef BLK_ANCHOR
 #define BLK_ANCHOR 44
 #endif
-constexpr int kAnchor = BLK_ANCHOR; // FP64 re-anchoring interval for e^{+-t} (nodes)
+constexpr int kAnchor = BLK_ANCHOR; // v1 loop: FP64 re-anchoring interval for e^{+-t} (nodes)
 #ifndef BLK_GROUP
 #define BLK_GROUP 4
 #endif
@@ -44,72 +34,67 @@ constexpr int kAnchor = BLK_ANCHOR; // FP64 re-anchoring interval for e^{+-t} (n
 #define BLK_MINB 6
 #endif
 constexpr int kGroup = BLK_GROUP; // nodes evaluated together (independent exp chains)
+#ifndef BLK_GROUP2
+#define BLK_GROUP2 4
+#endif
+constexpr int kGroup2 = BLK_GROUP2; // v2 loop group size
 
-__device__ __align__(16) const double kExp2Table[kExpTab] = {
-#include "exp2_table.inc"
+// 2^(j/2048) with (j << 9) subtracted from the high word (gen_exp2_table.py):
+// adding (k << 9) to the high word of entry k & 2047 gives 2^(k/2048) for
+// any k in [-2^21, 2^21) -- the 2^(k >> 11) scale costs one integer
+// multiply-add and no shift.
+__device__ __align__(16) const unsigned long long kExp2TablePc[kExpTab] = {
+#include "exp2_table_pc.inc"
 };
 
 // The shared-memory copy of the table, one per CTA of every kernel that
 // uses exp_tab.  A file-scope __shared__ array lets LDS address it with an
-// immediate offset (no base-register add per node).
-__shared__ __align__(16) double g_exp_tab[kTabSize];
+// immediate/uniform base (no per-node base-register add).
+__shared__ __align__(16) double g_exp_tab[kExpTab];
 
 // Block-cooperative copy of the table to shared memory (caller syncs).
-__device__ __forceinline__ void load_exp_table(double *tab = g_exp_tab) {
-  if (kTabRep == 1) {
-    const double2 *src = reinterpret_cast<const double2 *>(kExp2Table);
-    double2 *dst = reinterpret_cast<double2 *>(tab);
-    for (int j = threadIdx.x; j < kExpTab / 2; j += blockDim.x) dst[j] = src[j];
-  } else {
-    for (int j = threadIdx.x; j < kTabSize; j += blockDim.x) tab[j] = kExp2Table[j / kTabRep];
-  }
+__device__ __forceinline__ void load_exp_table() {
+  const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(kExp2TablePc);
+  ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(g_exp_tab);
+  for (int j = threadIdx.x; j < kExpTab / 2; j += blockDim.x) dst[j] = src[j];
 }
-// Table entry j for this lane (copy threadIdx.x % kTabRep): one LOP3 for
-// the caller's mask, one IMAD for the byte address, one LDS.64.
-__device__ __forceinline__ double exp_table_entry(int j) {
-  if (kTabRep != 1) return g_exp_tab[j * kTabRep + (int)(threadIdx.x % kTabRep)];
-  const unsigned base = (unsigned)__cvta_generic_to_shared(g_exp_tab);
-  unsigned addr;
-  asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(addr) : "r"((unsigned)j), "r"(base));
-  double val;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(val) : "r"(addr) : "memory");
-  return val;
-}
-// Kept for call sites that pass a table pointer; the shared table is global.
-__device__ __forceinline__ const double *lane_table(const double *tab) { return tab; }
 
-// exp(a) by Tang's table method: a = (k/2048) ln2 + r, |r| <= ln2/4096,
-// exp(a) = 2^(k>>11) * T[k&2047] * (1 + r + r^2/2 + r^3/6)   (truncation
-// r^4/24 < 3.5e-17).  Valid for a in [-707, 709]; CLAMP maps a < -707 to
-// e^-707 (caller decides whether its arguments can leave the range -- see
-// quad_f64).  7 FP64-pipe instructions + 1 LDS.64 + 4 integer ops.
-// hi + (n << 20) as one integer multiply-add (ptxas would otherwise rewrite
-// (k >> 11) << 20 as (k << 9) & mask and add: three instructions).
-__device__ __forceinline__ int add_exponent(int hi, int n) {
-  int r;
-  asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(r) : "r"(n), "r"(hi));
-  return r;
+// 2^(k/2048) for k in [-2^21, 2^21): one LDS.64 and one IMAD.
+__device__ __forceinline__ double exp_scale(int k) {
+  const double tj = g_exp_tab[k & (kExpTab - 1)];
+  return __hiloint2double(k * 512 + __double2hiint(tj), __double2loint(tj));
 }
+
 constexpr double kExpInvL = 2954.639443740597;       // 2048 / ln 2
 constexpr double kExpMagic = 6755399441055744.0;     // 1.5 * 2^52: round-to-int trick
 constexpr double kExpC = 0.0003384507717577858;      // ln2/2048 (single-step reduction:
                                                      // |k| <= 2.1e6 -> |error| < 6e-14 |a|/707)
-__device__ __forceinline__ double exp_poly_scale(double r, int k, double tj) {
+// e^r - 1 for |r| <= ln2/4096 (truncation r^4/24 < 3.5e-17): Horner, every
+// operation with at most two register operands (the FP64 pipe issues an
+// instruction reading three distinct 64-bit registers in 3 cycles, not 2:
+// two register-file banks).
+__device__ __forceinline__ double exp_em1(double r) {
   double p = fma(r, 1.6666666666666666e-01, 0.5);
-  p = fma(p, r * r, r);                               // e^r - 1
-  const double res = fma(tj, p, tj);
-  return __hiloint2double(add_exponent(__double2hiint(res), k >> kExpBits), __double2loint(res));
+  p = fma(p, r, 1.0);
+  return p * r;
 }
+
+// exp(a) by Tang's table method: a = (k/2048) ln2 + r, |r| <= ln2/4096,
+// exp(a) = 2^(k/2048) * (1 + em1(r)).  Valid for a in [-707, 709]; CLAMP maps
+// a < -707 to e^-707 (caller decides whether its arguments can leave the
+// range -- see quad_f64).  7 FP64-pipe instructions + LDS.64 + 3 integer ops.
 template <bool CLAMP>
-__device__ __forceinline__ double exp_tab(double a, const double *__restrict__ tab) {
+__device__ __forceinline__ double exp_tab(double a) {
   if (CLAMP) a = a < -707.0 ? -707.0 : a;
   double kd = fma(a, kExpInvL, kExpMagic);
   const int k = __double2loint(kd);
   kd -= kExpMagic;
   const double r = fma(kd, -kExpC, a);
-  (void)tab;
-  return exp_poly_scale(r, k, exp_table_entry(k & (kExpTab - 1)));
+  const double ts = exp_scale(k);
+  return fma(ts, exp_em1(r), ts);
 }
+template <bool CLAMP>
+__device__ __forceinline__ double exp_tab(double a, const double *) { return exp_tab<CLAMP>(a); }
 
 // 1/a to ~1 ulp: MUFU.RCP64H seed + two Newton steps.
 __device__ __forceinline__ double rcp64(double a) {
@@ -122,8 +107,8 @@ __device__ __forceinline__ double rcp64(double a) {
 }
 
 // 1 - e^z for z <= 0 without cancellation (-expm1(z)).
-__device__ __forceinline__ double one_minus_exp(double z, const double *__restrict__ tab) {
-  if (z < -0.34657359027997264) return 1.0 - exp_tab<true>(z, tab);
+__device__ __forceinline__ double one_minus_exp(double z) {
+  if (z < -0.34657359027997264) return 1.0 - exp_tab<true>(z);
   // Taylor series of -(e^z - 1) to z^14 (|z| <= ln2/2: truncation < 3e-18 |z|)
   double p = 1.0 / 87178291200.0;   // 1/14!
   p = fma(p, z, 1.0 / 6227020800.0);
@@ -170,45 +155,43 @@ __device__ __forceinline__ void accumulate(Sums64 &s, double E, double q, double
 // One node's contributions, given cosh t, q and p.
 template <bool DV, bool DX, bool HESS, bool CLAMP>
 __device__ __forceinline__ void node_acc(double v, double x, double s_mid, double t, double ch,
-                                         double q, double p, const double *__restrict__ tab,
-                                         Sums64 &s) {
-  accumulate<DV, DX, HESS>(s, exp_tab<CLAMP>(fma(-x, ch, fma(v, t, -s_mid)), tab), q, p, t, ch);
+                                         double q, double p, Sums64 &s) {
+  accumulate<DV, DX, HESS>(s, exp_tab<CLAMP>(fma(-x, ch, fma(v, t, -s_mid))), q, p, t, ch);
 }
 
-// Nodes [ib, ie) with weight 1.  Node positions are t0 + m h to 1 ulp (an
-// accumulated t += h would drift by m ulp, which v t amplifies for large v);
-// e^{+-t} are re-anchored every kAnchor nodes, q and p advance across chunks.
-// Nodes go in groups of kGroup whose exponentials are evaluated stage by
-// stage (independent dependency chains interleaved).
+// v1 node loop (general): nodes [ib, ie) with weight 1.  Node positions are
+// t0 + m h to 1 ulp (an accumulated t += h would drift by m ulp, which v t
+// amplifies for large v); e^{+-t} are re-anchored every kAnchor nodes, q and
+// p advance across chunks; p = 1 - q by an additive recurrence (no
+// cancellation for small v t, R21).  Used for the second-order sums, for
+// 0 < v < 1e-5 and for ranges that need the exp clamp.
 template <bool DV, bool DX, bool HESS, bool CLAMP>
 __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double h,
-                                           double s_mid, int ib, int ie,
-                                           const double *__restrict__ tab, Sums64 &out) {
+                                           double s_mid, int ib, int ie, Sums64 &out) {
   if (ie <= ib) return;
   constexpr bool NEEDP = DV || HESS;
   const double m2v = -2.0 * v;
-  const double eh = exp_tab<false>(h, tab);
+  const double eh = exp_tab<false>(h);
   const double ehi = rcp64(eh);
   const double tb = fma((double)ib, h, t0);
-  double q = exp_tab<true>(m2v * tb, tab);           // q_m = e^{-2 v t_m}
-  const double eq = exp_tab<true>(m2v * h, tab);
-  double p = NEEDP ? one_minus_exp(m2v * tb, tab) : 0.0;  // p_m = 1 - q_m
-  const double a1 = NEEDP ? one_minus_exp(m2v * h, tab) : 0.0;
+  double q = exp_tab<true>(m2v * tb);           // q_m = e^{-2 v t_m}
+  const double eq = exp_tab<true>(m2v * h);
+  double p = NEEDP ? one_minus_exp(m2v * tb) : 0.0;  // p_m = 1 - q_m
+  const double a1 = NEEDP ? one_minus_exp(m2v * h) : 0.0;
   Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  // chunks of kAnchor nodes (a multiple of kGroup), the last one shorter
   static_assert(kAnchor % kGroup == 0, "anchor interval must hold whole groups");
 #pragma unroll 1
   for (int c0 = ib; c0 < ie; c0 += kAnchor) {
     const int c1 = min(c0 + kAnchor, ie);
     double tc = fma((double)c0, h, t0);
-    double et = 0.5 * exp_tab<true>(fmin(tc, 709.0), tab);   // e^t / 2
-    double eti = 0.25 * rcp64(et);                           // e^-t / 2
+    double et = 0.5 * exp_tab<true>(fmin(tc, 709.0));   // e^t / 2
+    double eti = 0.25 * rcp64(et);                       // e^-t / 2
     if (c0 == 0) {
       // node 0 has weight 1/2: take half of it back.  It is exact
       // here (anchored state) and may be the largest node (t0 = 0 when the
       // peak region reaches t = 0), so this correction is done in FP64.
       Sums64 z{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      node_acc<DV, DX, HESS, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, z);
+      node_acc<DV, DX, HESS, CLAMP>(v, x, s_mid, tc, et + eti, q, p, z);
       s.S0 -= 0.5 * z.S0; s.S1 -= 0.5 * z.S1; s.S2 -= 0.5 * z.S2;
       s.S11 -= 0.5 * z.S11; s.S22 -= 0.5 * z.S22; s.S12 -= 0.5 * z.S12;
     }
@@ -229,7 +212,7 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
       }
       // the group's exponentials stage by stage, so consecutive dependent
       // FP64 instructions of one node are kGroup instructions apart
-      double a[kGroup], kd[kGroup], r[kGroup], pp[kGroup], tj[kGroup];
+      double a[kGroup], kd[kGroup], r[kGroup], ts[kGroup];
       int k[kGroup];
 #pragma unroll
       for (int j = 0; j < kGroup; ++j) a[j] = fma(v, tg[j], -s_mid);
@@ -246,25 +229,19 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
         kd[j] -= kExpMagic;
       }
 #pragma unroll
-      for (int j = 0; j < kGroup; ++j) tj[j] = exp_table_entry(k[j] & (kExpTab - 1));
+      for (int j = 0; j < kGroup; ++j) ts[j] = exp_scale(k[j]);
 #pragma unroll
       for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
 #pragma unroll
-      for (int j = 0; j < kGroup; ++j) pp[j] = fma(r[j], 1.6666666666666666e-01, 0.5);
-#pragma unroll
-      for (int j = 0; j < kGroup; ++j) pp[j] = fma(pp[j], r[j] * r[j], r[j]);
-#pragma unroll
       for (int j = 0; j < kGroup; ++j) {
-        const double res = fma(tj[j], pp[j], tj[j]);
-        const double E = __hiloint2double(add_exponent(__double2hiint(res), k[j] >> kExpBits),
-                                          __double2loint(res));
+        const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
         accumulate<DV, DX, HESS>(s, E, qg[j], pg[j], tg[j], chg[j]);
       }
       tc = fma((double)(m + kGroup), h, t0);
     }
 #pragma unroll 1
     for (; m < c1; ++m) {                            // remainder
-      node_acc<DV, DX, HESS, CLAMP>(v, x, s_mid, tc, et + eti, q, p, tab, s);
+      node_acc<DV, DX, HESS, CLAMP>(v, x, s_mid, tc, et + eti, q, p, s);
       if (NEEDP) p = fma(q, a1, p);
       q *= eq;
       et *= eh; eti *= ehi;
@@ -273,6 +250,101 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
   }
   out.S0 += s.S0; out.S1 += s.S1; out.S2 += s.S2;
   out.S11 += s.S11; out.S22 += s.S22; out.S12 += s.S12;
+}
+
+// v2 node loop (first-order sums, no exp clamp, v = 0 or v >= 1e-5):
+// the same nodes and sums, arranged so that almost every FP64 instruction
+// reads at most two distinct 64-bit registers (a third costs
+// a full extra issue cycle on B200):
+//   * x is folded into the cosh recurrence: X = x cosh t = Xp + Xm with
+//     Xp = (x/2) e^t, Xm = (x/2) e^{-t}; S2 is accumulated as sum w X and
+//     divided by x once at the end;
+//   * v t - s = B_j = B_c + j (v h) from the group base B_c = v t_c - s
+//     (immediate j), so the exponent is a = B_j - X_j;
+//   * E t p = E (1 - q) t with E (1 - q) = 2E - w (w = E (1 + q)); for
+//     v >= 1e-5 the cancellation costs < 2 eps/(2 v t) relative on a node
+//     whose term is itself ~2 v t of E t, i.e. < 1e-11 of S1 (v = 0 gives
+//     exactly 0); smaller v takes the v1 loop;
+//   * e^{+-t} and q advance per group by e^{+-G h}, e^{-2 v G h} and inside
+//     the group by e^{+-h}, e^{-2 v h}: drift <= n/G + G ulp, no re-anchoring.
+template <bool DV, bool DX>
+__device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, double h,
+                                              double s_mid, int ib, int ie, Sums64 &out) {
+  if (ie <= ib) return;
+  constexpr int G = kGroup2;
+  const double vh = v * h;
+  const double m2v = -2.0 * v;
+  const double tb = fma((double)ib, h, t0);
+  const double eb = exp_tab<true>(fmin(tb, 709.0));
+  const double hx = 0.5 * x;
+  double XpG = hx * eb, XmG = hx * rcp64(eb);
+  const double e1 = exp_tab<false>(h), e1i = rcp64(e1);
+  const double eG = exp_tab<true>(fmin(G * h, 709.0)), eGi = rcp64(eG);
+  double qG = exp_tab<true>(m2v * tb);
+  const double eq1 = exp_tab<true>(m2v * h), eqG = exp_tab<true>(m2v * (G * h));
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+  if (ib == 0) {
+    // node 0 carries weight 1/2: take half of it back (exact state)
+    const double E = exp_tab<false>(fma(v, t0, -s_mid) - (XpG + XmG));
+    const double w = fma(E, qG, E);
+    S0 = -0.5 * w;
+    if (DX) S2 = -0.5 * (w * (XpG + XmG));
+    if (DV) S1 = -0.5 * (fma(E, 2.0, -w) * t0);
+  }
+  double md = (double)ib;
+  int m = ib;
+#pragma unroll 1
+  for (; m + G <= ie; m += G) {
+    const double tc = fma(md, h, t0);
+    md += (double)G;
+    const double Bc = fma(v, tc, -s_mid);
+    double X[G], a[G], q[G], kd[G], r[G], ts[G];
+    int k[G];
+    double xp = XpG, xm = XmG, qq = qG;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      X[j] = xp + xm;
+      q[j] = qq;
+      if (j + 1 < G) { xp *= e1; xm *= e1i; qq *= eq1; }
+    }
+    XpG *= eG; XmG *= eGi; qG *= eqG;
+#pragma unroll
+    for (int j = 0; j < G; ++j) a[j] = (j == 0 ? Bc : fma(double(j), vh, Bc)) - X[j];
+#pragma unroll
+    for (int j = 0; j < G; ++j) kd[j] = fma(a[j], kExpInvL, kExpMagic);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      k[j] = __double2loint(kd[j]);
+      kd[j] -= kExpMagic;
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) ts[j] = exp_scale(k[j]);
+#pragma unroll
+    for (int j = 0; j < G; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
+      const double w = fma(E, q[j], E);
+      S0 += w;
+      if (DX) S2 = fma(w, X[j], S2);
+      if (DV) S1 = fma(fma(E, 2.0, -w), j == 0 ? tc : fma(double(j), h, tc), S1);
+    }
+  }
+  double xp = XpG, xm = XmG, qq = qG;
+#pragma unroll 1
+  for (; m < ie; ++m) {                             // remainder, one node at a time
+    const double t = fma((double)m, h, t0);
+    const double X = xp + xm;
+    const double E = exp_tab<false>(fma(v, t, -s_mid) - X);
+    const double w = fma(E, qq, E);
+    S0 += w;
+    if (DX) S2 = fma(w, X, S2);
+    if (DV) S1 = fma(fma(E, 2.0, -w), t, S1);
+    xp *= e1; xm *= e1i; qq *= eq1;
+  }
+  out.S0 += S0;
+  if (DV) out.S1 += S1;
+  if (DX) out.S2 += S2 * rcp64(x);
 }
 
 // Half of the last node's contributions, evaluated in FP32: that node sits
@@ -311,7 +383,13 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
                                            const double *__restrict__ tab) {
   Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double s_mid = shift + kLn2;                 // E = exp(vt - x cosh t - s_mid)
-  nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, tab, s);
+  (void)tab;
+#ifndef BLK_QUAD_V1
+  if (!HESS && !CLAMP && !(v > 0.0 && v < 1e-5))
+    nodes_fp64_v2<DV, DX>(v, x, t0, h, s_mid, mb, me, s);
+  else
+#endif
+    nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, s);
   // node n: t_n = t1 lies outside the eps-support (d(t1) < 0, FindZero
   // returns the outer end, R1), so its term is < 2^-52 of the peak term
   if (me == n + 1) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
