@@ -66,7 +66,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64);
+      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
@@ -124,7 +124,7 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64);
+      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
@@ -175,7 +175,7 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32<true>(v, x, kLogEpsF32);
+      const Plan<float> p = make_plan_f32<true>(v, x, kLogEpsF32, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);

@@ -48,7 +48,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
       double t0, t1, gp, dmin;
       bool ok;
       if (f32_plan_domain(1.0, z)) {
-        const Plan<float> p = make_plan_f32(1.0, z, kLogEpsF64);
+        const Plan<float> p = make_plan_f32(1.0, z, kLogEpsF64, fz_tol_for(nbins));
         ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
       } else {
         const Plan<double> p = make_plan_f64(1.0, z, kLogEpsF64);

@@ -183,12 +183,30 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 
 using PlanF32 = PlanF32T<false>;
 
-// Alg. 2 with the two evaluations packed into f32x2 operations.
+// Alg. 2 with the two evaluations packed into f32x2 operations.  The loop
+// ends after max_iter = 10 iterations or earlier, per the paper's
+// "until" clause, once the Newton correction from the kept end a is
+// below kFzTolRel of |a|: a is then within that distance of the zero and
+// still on its outer side (F(a) < 0 is kept invariant), so the range stays
+// conservative; it is at most ~2^-10 relative wider than after 10 iterations,
+// which changes no output beyond rounding (R4, R20).  The literal
+// tol = 1 on |a_i - a_{i-1}| is not used (R4: it stops on the first
+// iteration that keeps a, and breaks config 3).
+// The tolerance follows the grid: with nbins >= 32 the trapezoid error is at
+// rounding level and insensitive to the range (R20), so 2^-10; coarser grids
+// are sensitive to where the nodes fall, so 2^-20 (FP32 resolution).
+__host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
+  return nbins >= 32 ? 9.765625e-4f : 9.5367431640625e-7f;
+}
 template <bool PEAK, bool ASC, class PF>
 __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
-                                               float dFa, float b) {
+                                               float dFa, float b, float tol) {
 #pragma unroll 2
   for (int i = 0; i < kMaxIter; ++i) {
+    // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
+    // carries no information and must not end the search)
+    const float rhs = tol * fabsf(a * dFa);
+    if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
     float mid, tn;
     fz_points_f32<ASC>(a, Fa, dFa, b, mid, tn);
     float2 F, dF;
@@ -221,7 +239,8 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 // Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
 // is taken in double on the caller's inputs.
 template <bool NEWTON = false>
-__device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps) {
+__device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps,
+                                                    float tol) {
   Plan<float> p;
   PlanF32T<NEWTON> P;
   P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
@@ -232,16 +251,16 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   if (vd * vd - xd > 0.0) {
     auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
     if (!find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
-    p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo);  // (t_e, t_s)
+    p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo, tol);  // (t_e, t_s)
   }
   p.gp = P.gval(p.tp);
   const float c = p.gp + P.L + float(kLn2);
   p.t0 = 0.0f;
   float d0 = -P.x - p.gp - P.L;                                    // d(0)
-  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp);
+  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp, tol);
   auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
   if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
-  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo);
+  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol);
   p.dmin = fminf(d0, Fh);
   p.ok = true;
   return p;

@@ -28,7 +28,7 @@ plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   bool ok = false;
   if (valid) {
     if (range_mode == 0 && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64);
+      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
