@@ -36,13 +36,15 @@ import numpy as np  # noqa: E402
 
 import workloads  # noqa: E402
 
-# Per-element FP64 work of the fused kernel (DFMA counted as 2 flops, DADD/DMUL
-# as 1), measured with ncu on config c2 at nbins=128 (profiles/r01_*; DESIGN.md
-# §6).  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
-FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4356.3}
+# Per-element FP64 work of the fused kernel's algorithm (DFMA counted as 2
+# flops, DADD/DMUL as 1): the FP64 operations the kernel executes per element
+# (ncu sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on over one
+# launch / n) on config c2 at nbins=128 -- profiles/r01_p3_ncu_full_summary.txt,
+# DESIGN.md §5.  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
+FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4063.0}
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch (same capture),
 # per element; the outputs stay in L2 until after the kernel.
-DRAM_BYTES_PER_ELEMENT = {("c2", 128): 16.08}
+DRAM_BYTES_PER_ELEMENT = {("c2", 128): 16.09}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2
 
 
@@ -103,14 +105,20 @@ def oracle_rate(cfg, nbins, seconds, threads):
     oracle.logk(v.astype(np.float64), x.astype(np.float64), nbins, threads=threads)
     probe = time.perf_counter() - t
     per = probe / 2048
-    n = int(min(workloads.CONFIGS[cfg].n, max(4096, seconds / per * threads * 0.9)))
+    want = max(4096, int(seconds / per * threads * 0.9))
+    n = int(min(workloads.CONFIGS[cfg].n, want, 1 << 22))
     v, x = workloads.generate(cfg, 0, n)
     v = v.astype(np.float64)
     x = x.astype(np.float64)
-    t = time.perf_counter()
-    oracle.logk(v, x, nbins, threads=threads)
-    dt = time.perf_counter() - t
-    return n / dt, n, dt
+    # repeat passes over the prefix sample until ~`seconds` of CPU work
+    passes, t = 0, time.perf_counter()
+    while True:
+        oracle.logk(v, x, nbins, threads=threads)
+        passes += 1
+        dt = time.perf_counter() - t
+        if dt >= seconds * 0.9 or passes * n >= want:
+            break
+    return passes * n / dt, passes * n, dt
 
 
 class ClockSampler:
@@ -352,7 +360,8 @@ def main():
         cores, model = cpu_info()
         r, ns, secs = oracle_rate(args.config, args.nbins, args.cpu_seconds, cores)
         cpu = {"value": r, "unit": "evals/s", "cores": cores, "kind": "oracle",
-               "sample": f"first {ns} elements of {args.config} ({secs:.1f} s, {cores} threads, {model})"}
+               "sample": f"{ns} evaluations over the first {min(ns, workloads.CONFIGS[args.config].n, 1 << 22)} "
+                          f"elements of {args.config} ({secs:.1f} s, {cores} threads, {model})"}
 
     line = {
         "metric": "logK+dv+dx evals/sec FP64" if dt == torch.float64 else "logK+dv+dx evals/sec FP32",

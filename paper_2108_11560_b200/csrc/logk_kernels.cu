@@ -325,6 +325,11 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
   return BLK_OK;
 }
 
+#ifdef BLK_MIN_INSTANCES
+// tuning-variant builds (tools/build_variants.py): one element per lane only
+#define BLK_DISPATCH_LPE(KER, L, O1, O2, O3) \
+  return launch_k(KER<O1, O2, O3, 1>, n, 1, th, stream, v, x, a, b, c, nbins, mode);
+#else
 #define BLK_DISPATCH_LPE(KER, L, O1, O2, O3)                                        \
   switch (L) {                                                                      \
     case 1: return launch_k(KER<O1, O2, O3, 1>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
@@ -334,6 +339,7 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
     case 16: return launch_k(KER<O1, O2, O3, 16>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
     default: return launch_k(KER<O1, O2, O3, 32>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
   }
+#endif
 
 template <class K>
 blk_status launch_ws(K kern, size_t n, cudaStream_t st, const double *v, const double *x,
