@@ -26,6 +26,33 @@ namespace blk {
 
 constexpr int kDefaultThreads = 128;
 
+#ifdef BLK_TIMELINE
+// Diagnostic build only (tools/build_variants.py ...=BLK_TIMELINE): per-warp
+// %globaltimer stamps (start, plan done, end) and SM id of the FP64 kernel.
+constexpr int kTlMax = 1 << 16;
+__device__ unsigned long long g_tl[kTlMax][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define BLK_TL(slot)                                                              \
+  do {                                                                            \
+    const unsigned w_ = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;             \
+    if ((threadIdx.x & 31) == 0 && w_ < kTlMax) {                                 \
+      g_tl[w_][slot] = gtimer();                                                  \
+      if (slot == 0) g_tl[w_][3] = smid();                                        \
+    }                                                                             \
+  } while (0)
+#else
+#define BLK_TL(slot) do {} while (0)
+#endif
+
 template <int LPE, class T>
 __device__ __forceinline__ T group_sum(T a) {
 #pragma unroll
@@ -46,6 +73,7 @@ __global__ void __launch_bounds__(128, BLK_MINB)
 logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 double *__restrict__ logk, double *__restrict__ dlogk_dv,
                 double *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  BLK_TL(0);
   load_exp_table();
   __syncthreads();
   const double *tab = g_exp_tab;
@@ -74,6 +102,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
+  BLK_TL(1);
   // a6: fixed-bin quadrature, three sums in one pass
   Sums64 s{0.0, 0.0, 0.0};
   const double h = (t1 - t0) * rcp64((double)nbins);   // h = (t1 - t0)/n
@@ -90,6 +119,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
     if (DV) s.S1 = group_sum<LPE>(s.S1);
     if (DX) s.S2 = group_sum<LPE>(s.S2);
   }
+  BLK_TL(2);
   if (!live || sub != 0) return;
   // a7: epilogue
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
@@ -600,6 +630,14 @@ blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, doubl
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BLK_OK : cuda_fail(e, "split kernels");
 }
+
+#ifdef BLK_TIMELINE
+__attribute__((visibility("default"))) blk_status blk_debug_timeline(unsigned long long *host, size_t max_warps) {
+  const size_t n = max_warps < (size_t)blk::kTlMax ? max_warps : (size_t)blk::kTlMax;
+  cudaError_t e = cudaMemcpyFromSymbol(host, blk::g_tl, n * 4 * sizeof(unsigned long long));
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "timeline copy");
+}
+#endif
 
 blk_status blk_microbench_fp64(int blocks, int threads, int iters, double *out, cudaStream_t s) {
   if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out)

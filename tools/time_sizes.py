@@ -40,10 +40,25 @@ def main():
     vt = torch.from_numpy(v).to(dev).repeat(reps)[:nmax]
     xt = torch.from_numpy(x).to(dev).repeat(reps)[:nmax]
     o = [torch.empty_like(vt) for _ in range(3)]
+    import ctypes
+    L = blk.lib()
+    f = L.blk_debug_split_f64
+    f.restype = ctypes.c_int
+    vp = ctypes.c_void_p
+    f.argtypes = [vp, vp, ctypes.c_size_t, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int, vp]
+    scratch = torch.empty(nmax * 32, dtype=torch.uint8, device=dev)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = [ctypes.c_void_p(t.data_ptr()) for t in (vt, xt, *o, scratch)]
+    split = "--split" in os.environ.get("TS_OPTS", "")
     for n in sizes:
         ms = timeit(lambda: blk.bessel_logk_f64(vt[:n], xt[:n], o[0][:n], o[1][:n], o[2][:n], nbins=128))
-        print(f"{cfg} n={n:9d} waves={n / (6 * 148 * 128):6.2f} {ms:.4f} ms  {n / ms * 1e3:.3e} evals/s",
-              flush=True)
+        line = f"{cfg} n={n:9d} waves={n / (6 * 148 * 128):6.2f} fused {ms:.4f} ms  {n / ms * 1e3:.3e} evals/s"
+        if split:
+            f(P[0], P[1], n, P[2], P[3], P[4], 128, P[5], 1, s)
+            mp = timeit(lambda: f(P[0], P[1], n, P[2], P[3], P[4], 128, P[5], 1, s))
+            mq = timeit(lambda: f(P[0], P[1], n, P[2], P[3], P[4], 128, P[5], 2, s))
+            line += f" | plan {mp:.4f} ms quad {mq:.4f} ms"
+        print(line, flush=True)
 
 
 if __name__ == "__main__":
