@@ -67,6 +67,9 @@ def _load():
                 f = getattr(lib, name)
                 f.restype = ctypes.c_double
                 f.argtypes = [ctypes.c_double] * 3
+            lib.oracle_logk_own_range.restype = ctypes.c_int
+            lib.oracle_logk_own_range.argtypes = [dp, dp, ctypes.c_size_t, dp, dp, dp,
+                                                  ctypes.c_int, ctypes.c_double]
             lib.oracle_log_eps_f64.restype = ctypes.c_double
             lib.oracle_log_eps_f32.restype = ctypes.c_double
             _lib = lib
@@ -129,6 +132,31 @@ def logk(v, x, nbins: int = 128, *, max_iter: int = MAX_ITER, tol: float = 0.0,
                         range(threads)))
     if with_plan:
         return out[0], out[1], out[2], plan
+    return out[0], out[1], out[2]
+
+
+def logk_own_range(v, x, nbins: int = 128, threads: int = 1):
+    """log K, dlogK/dv, dlogK/dx with each derivative integrand f^{(1,0)},
+    f^{(0,1)} integrated over ITS OWN range (Sec. 4.1) --
+    the cross-check of reading R14 (the hot path shares f's range)."""
+    lib = _load()
+    v = _as_f64(v).ravel()
+    x = _as_f64(x).ravel()
+    n = v.size
+    out = [np.empty(n), np.empty(n), np.empty(n)]
+
+    def run(lo, hi):
+        if hi > lo:
+            lib.oracle_logk_own_range(v.ctypes.data + 8 * lo, x.ctypes.data + 8 * lo, hi - lo,
+                                      out[0].ctypes.data + 8 * lo, out[1].ctypes.data + 8 * lo,
+                                      out[2].ctypes.data + 8 * lo, int(nbins), log_eps_f64())
+
+    if threads <= 1 or n < 1024:
+        run(0, n)
+    else:
+        bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda k: run(int(bounds[k]), int(bounds[k + 1])), range(threads)))
     return out[0], out[1], out[2]
 
 

@@ -41,6 +41,7 @@ typedef struct {
     double x;   /* argument, x > 0 */
     double gp;  /* g(t_p), set once t_p is known */
     double L;   /* log(eps) (R8/R9) */
+    int dn, dm; /* derivative integrand f^{(n,m)} of Sec. 4.1 (oracle_logk_own_range) */
 } oracle_ctx;
 
 /* log cosh(z), z >= 0, in the overflow-free form z + log1p(e^{-2z}) - log 2
@@ -232,6 +233,69 @@ static void oracle_one_h(double v_in, double x, int nbins, int max_iter, double 
     }
 }
 
+/*
+ * Sec. 4.1: the derivative integrands, each with ITS OWN range.
+ * log (-1)^m f^{(n,m)}(t) = n log t + m log cosh t + log cosh(vt)  (n even)
+ *                                                  + log sinh(vt)  (n odd)
+ *                           - x cosh t                               (R13)
+ * "and these also have the single range that should be integrated as the
+ * f case": the same Alg. 1-3 on this log-integrand.  Used only as
+ * the cross-check of R14 (the hot path shares f's range and nodes).
+ */
+static double gn0(const oracle_ctx *c, double t)
+{
+    double r = (c->dn ? c->dn * log(t) : 0.0) + c->dm * log_cosh(t) - c->x * cosh(t);
+    if (c->dn % 2 == 0) return r + log_cosh(c->v * t);
+    double z = c->v * t;                     /* log sinh z, overflow-free (z > 0) */
+    return r + z + log(-expm1(-2.0 * z)) - M_LN2;
+}
+static double gn1(const oracle_ctx *c, double t)
+{
+    double r = (c->dn ? c->dn / t : 0.0) + c->dm * tanh(t) - c->x * sinh(t);
+    if (c->dn % 2 == 0) return r + c->v * tanh(c->v * t);
+    return r + c->v / tanh(c->v * t);
+}
+static double gn2(const oracle_ctx *c, double t)
+{
+    double ch = cosh(t), cv = cosh(c->v * t), sv = sinh(c->v * t);
+    double r = (c->dn ? -c->dn / (t * t) : 0.0) + c->dm / (ch * ch) - c->x * ch;
+    if (c->dn % 2 == 0) return r + c->v * c->v / (cv * cv);
+    return r - c->v * c->v / (sv * sv);
+}
+static double dnfun(const oracle_ctx *c, double t)
+{
+    return gn0(c, t) - c->gp - c->L;
+}
+
+/* log of int_0^inf |f^{(n,m)}(t)| dt by Alg. 3 + Eq. (int) on its own range.
+ * The peak test of P:257 generalises to "g' > 0 just right of 0": for n >= 1
+ * g -> -inf at 0+ (always an interior peak); for n = 0 it is g''(0) > 0,
+ * i.e. m + v^2 - x > 0.  Returns NaN when the plan fails. */
+static double oracle_log_int_nm(double v, double x, int dn, int dm, int nbins, double log_eps)
+{
+    oracle_ctx c = { v, x, 0.0, log_eps, dn, dm };
+    double lo, hi, tp = 0.0;
+    int peaked = (dn > 0) ? 1 : (dm + v * v - x > 0.0);
+    if (peaked) {
+        if (find_range(&c, gn1, 0.0, &lo, &hi) != 0) return NAN;
+        tp = find_zero(&c, gn1, gn2, hi, lo, 10, 0.0);
+    }
+    c.gp = gn0(&c, tp);
+    double t0 = 0.0;
+    if (!(gn0(&c, 0.0) - c.gp > c.L))            /* d(0) <= 0 (or -inf for n >= 1) */
+        t0 = find_zero(&c, dnfun, gn1, 0.0, tp, 10, 0.0);
+    if (find_range(&c, dnfun, tp, &lo, &hi) != 0) return NAN;
+    double t1 = find_zero(&c, dnfun, gn1, hi, lo, 10, 0.0);
+    double h = (t1 - t0) / nbins, S = 0.0;
+    for (int k = 0; k <= nbins; ++k) {
+        double t = t0 + k * h;
+        double cm = (k == 0 || k == nbins) ? 0.5 : 1.0;
+        double e = gn0(&c, t) - c.gp;
+        if (isfinite(e)) S += cm * exp(e);       /* the t = 0 node of n >= 1 is 0 */
+    }
+    return c.gp + log(h) + log(S);
+}
+
 /* ---------------- exported (C ABI, loaded by tests via ctypes) ------------- */
 
 /* log(2^-52): eps = DBL_EPSILON, R9 */
@@ -312,6 +376,36 @@ int oracle_logk_literal_cm(const double *v, const double *x, size_t n,
             S += h * exp(cm * (g0(&c, t) - c.gp));
         }
         logk[i] = c.gp + log(S);
+    }
+    return 0;
+}
+
+/*
+ * Cross-check of R14: d log K/dv and d log K/dx from the derivative
+ * integrands f^{(1,0)}, f^{(0,1)} integrated over their OWN ranges:
+ *   dlogK/dv = sign(v) exp(log I10 - log K),  dlogK/dx = -exp(log I01 - log K),
+ * log K from f's own plan as in oracle_logk.  v = 0 gives dv = 0 (f^{(1,0)} = 0).
+ */
+int oracle_logk_own_range(const double *v, const double *x, size_t n, double *logk,
+                          double *dlogk_dv, double *dlogk_dx, int nbins, double log_eps)
+{
+    if (nbins < 1)
+        return -1;
+    for (size_t i = 0; i < n; ++i) {
+        double lk, b, d;
+        oracle_one(v[i], x[i], nbins, 10, 0.0, log_eps, &lk, &b, &d, NULL);
+        if (logk) logk[i] = lk;
+        double av = fabs(v[i]), s = (v[i] < 0.0) ? -1.0 : 1.0;
+        if (!isfinite(lk)) {
+            if (dlogk_dv) dlogk_dv[i] = NAN;
+            if (dlogk_dx) dlogk_dx[i] = NAN;
+            continue;
+        }
+        if (dlogk_dv)
+            dlogk_dv[i] = (av == 0.0) ? 0.0
+                          : s * exp(oracle_log_int_nm(av, x[i], 1, 0, nbins, log_eps) - lk);
+        if (dlogk_dx)
+            dlogk_dx[i] = -exp(oracle_log_int_nm(av, x[i], 0, 1, nbins, log_eps) - lk);
     }
     return 0;
 }

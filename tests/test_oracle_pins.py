@@ -358,3 +358,27 @@ def test_hess_vs_brute_force(cfg):
     assert np.all(np.abs(dvv - bvv) <= 1e-13 * (np.abs(bvv) + dv * dv) + 1e-15)
     assert np.all(np.abs(dxx - bxx) <= 1e-13 * (np.abs(bxx) + dx * dx) + 1e-15)
     assert np.all(np.abs(dvx - bvx) <= 1e-13 * (np.abs(bvx) + np.abs(dv * dx)) + 1e-15)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_reading_R14_own_range_derivatives(cfg):
+    """R14: the paper integrates each derivative integrand f^{(n,m)} over its OWN
+    range (Sec. 4.1); the hot path shares f's range and nodes.  The
+    oracle implements both; they agree to rounding (relative 2e-14 of max(1,|log K|):
+    exp(log I - log K) carries eps*|log K|), and the own-range result is itself
+    pinned to the long-double brute force."""
+    v, x = workloads.generate(cfg, 0, 1500)
+    v = v.astype(np.float64)
+    x = x.astype(np.float64)
+    lk, dv, dx = oracle.logk(v, x, 128)
+    lk2, dv2, dx2 = oracle.logk_own_range(v, x, 128)
+    assert np.array_equal(lk, lk2)
+    sc = np.maximum(1.0, np.abs(lk))
+    nz = dv != 0
+    assert np.all(dv2[~nz] == 0.0)
+    assert np.all(np.abs(dv2[nz] - dv[nz]) <= 2e-14 * sc[nz] * np.abs(dv[nz]))
+    assert np.all(np.abs(dx2 - dx) <= 2e-14 * sc * np.abs(dx))
+    bl, bv, bx = oracle.brute(v[:120], x[:120], threads=os.cpu_count() or 1)
+    nzb = bv != 0
+    assert np.all(np.abs(dv2[:120][nzb] - bv[nzb]) <= 5e-14 * sc[:120][nzb] * np.abs(bv[nzb]))
+    assert np.all(np.abs(dx2[:120] - bx) <= 5e-14 * sc[:120] * np.abs(bx))
