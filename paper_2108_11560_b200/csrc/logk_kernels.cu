@@ -25,6 +25,9 @@
 namespace blk {
 
 constexpr int kDefaultThreads = 128;
+#ifndef BLK_F32_NEWTON
+#define BLK_F32_NEWTON false  // FP32 entry point plan: 1/(1+q) by MUFU.RCP (Newton steps on the FMA pipe measured no faster)
+#endif
 
 #ifdef BLK_TIMELINE
 // Diagnostic build only (tools/build_variants.py ...=BLK_TIMELINE): per-warp
@@ -201,15 +204,15 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   const float v = fabsf(vraw);
   const float sgn = (vraw < 0.0f) ? -1.0f : 1.0f;
 
-  float t0 = 0.0f, t1 = 0.0f, gp = 0.0f;
+  float t0 = 0.0f, t1 = 0.0f, gp = 0.0f, dmin = 0.0f;
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32<true>(v, x, kLogEpsF32, fz_tol_for(nbins));
-      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp;
+      const Plan<float> p = make_plan_f32<BLK_F32_NEWTON>(v, x, kLogEpsF32, fz_tol_for(nbins));
+      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);
-      ok = p.ok; t0 = (float)p.t0; t1 = (float)p.t1; gp = (float)p.gp;
+      ok = p.ok; t0 = (float)p.t0; t1 = (float)p.t1; gp = (float)p.gp; dmin = (float)p.dmin;
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
@@ -218,7 +221,14 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   if (ok) {
     int mb, me;
     lane_bins<LPE>(nbins, sub, mb, me);
-    s = quad_f32<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
+    // the fixed-point exponent needs every node within 2^-126 of the peak:
+    // true when both range ends are < 60 below the log-eps level (always on
+    // ranges found by Alg. 1-3; kept exact for safety)
+#ifndef BLK_F32_V1
+    if (dmin > -60.0f) s = quad_f32_v2<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
+    else
+#endif
+      s = quad_f32<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
   }
   if (LPE > 1) {
     s.S0 = group_sum<LPE>(s.S0);
