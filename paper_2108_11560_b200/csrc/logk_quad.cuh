@@ -261,10 +261,11 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
 //     divided by x once at the end;
 //   * v t - s = B_j = B_c + j (v h) from the group base B_c = v t_c - s
 //     (immediate j), so the exponent is a = B_j - X_j;
-//   * E t p = E (1 - q) t with E (1 - q) = 2E - w (w = E (1 + q)); for
-//     v >= 1e-5 the cancellation costs < 2 eps/(2 v t) relative on a node
-//     whose term is itself ~2 v t of E t, i.e. < 1e-11 of S1 (v = 0 gives
-//     exactly 0); smaller v takes the v1 loop;
+//   * E t p = E (1 - q) t with E (1 - q) = 2E - w (w = E (1 + q)): the
+//     rounding of w costs ~eps/(2 v t_w) of S1 (t_w the weighted mean node
+//     position, >= t1/2 here), so the caller takes this loop only when
+//     v t1 >= 1e-3 (error < 3e-13) or v = 0 (exactly 0); smaller v t1 takes
+//     the v1 loop;
 //   * e^{+-t} and q advance per group by e^{+-G h}, e^{-2 v G h} and inside
 //     the group by e^{+-h}, e^{-2 v h}: drift <= n/G + G ulp, no re-anchoring.
 template <bool DV, bool DX>
@@ -385,7 +386,7 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
   const double s_mid = shift + kLn2;                 // E = exp(vt - x cosh t - s_mid)
   (void)tab;
 #ifndef BLK_QUAD_V1
-  if (!HESS && !CLAMP && !(v > 0.0 && v < 1e-5))
+  if (!HESS && !CLAMP && !(v > 0.0 && v * fma((double)n, h, t0) < 1e-3))
     nodes_fp64_v2<DV, DX>(v, x, t0, h, s_mid, mb, me, s);
   else
 #endif

@@ -321,3 +321,33 @@ def test_parity_hessian(cfg, lanes):
     # the Bessel ODE on the GPU outputs directly
     ode = 1 + v * v / (x * x) - got[2] / x - got[2] ** 2
     assert np.all(np.abs(got[4] - ode) <= 1e-11 * (np.abs(ode) + got[2] ** 2 + v * v / (x * x) + 1))
+
+
+def test_loop_switch_small_order():
+    """The FP64 quadrature takes the v2 loop (S1 from 2E - w) for v = 0 and
+    v t1 >= 1e-3 and the general loop (additive p = 1 - q) below (DESIGN.md
+    §5): both sides of the switch, incl. large x (short ranges, small t1),
+    stay within the FP64 tolerance."""
+    v = np.repeat([0.0, 1e-12, 1e-8, 9.99e-6, 1.0e-5, 1.01e-5, 1e-4, 1e-3, 1e-2], 7)
+    x = np.tile([1e-2, 0.1, 1.0, 3.0, 10.0, 100.0, 1000.0], 9)
+    for dt in (np.float64,):
+        got = run_gpu(v.astype(dt), x.astype(dt))
+        ref = run_oracle(v, x)
+        assert_parity(got, ref, "f64", "small order")
+        assert np.all(got["dv"][v == 0] == 0.0)
+        # d/dv log K -> 0 like v: the relative error must not blow up as v -> 0
+        nz = v > 0
+        rel = np.abs(got["dv"][nz] - ref["dv"][nz]) / np.abs(ref["dv"][nz])
+        assert rel.max() <= 1e-10
+
+
+def test_f32_fixed_point_exponent_edges():
+    """FP32 entry point: the fixed-point exponent path (dmin > -60) and its
+    fallback give FP32-tolerance results across the whole c4 domain corner
+    set, incl. tiny/huge x and v = 0."""
+    v = np.repeat(np.array([0.0, 1e-6, 0.5, 5.0, 25.0, 50.0], np.float32), 6)
+    x = np.tile(np.array([1e-2, 0.05, 1.0, 10.0, 60.0, 100.0], np.float32), 6)
+    got = run_gpu(v, x)
+    ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
+    assert_parity(got, ref, "f32", "f32 edges")
+    assert np.all(got["dv"][v == 0] == 0.0)
