@@ -268,7 +268,29 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
 //     the v1 loop;
 //   * e^{+-t} and q advance per group by e^{+-G h}, e^{-2 v G h} and inside
 //     the group by e^{+-h}, e^{-2 v h}: drift <= n/G + G ulp, no re-anchoring.
-template <bool DV, bool DX>
+// One node of the v2 loop: E = e^{a}, w = E (1 + q), Ep = 2E - w = E (1 - q)
+// (S1 term / t), X = x cosh t.  HESS adds the second-order sums in the
+// scaled form S22x = sum w X^2 = x^2 S22 and S12x = sum Ep t X = x S12.
+template <bool DV, bool DX, bool HESS>
+__device__ __forceinline__ void v2_accumulate(double E, double q, double X, double t, double &S0,
+                                              double &S1, double &S2, double &S11, double &S22,
+                                              double &S12) {
+  const double w = fma(E, q, E);
+  S0 += w;
+  if (HESS) {
+    const double wX = w * X, wt = w * t, ept = fma(E, 2.0, -w) * t;
+    S2 += wX;
+    S22 = fma(wX, X, S22);
+    S11 = fma(wt, t, S11);
+    S1 += ept;
+    S12 = fma(ept, X, S12);
+  } else {
+    if (DX) S2 = fma(w, X, S2);
+    if (DV) S1 = fma(fma(E, 2.0, -w), t, S1);
+  }
+}
+
+template <bool DV, bool DX, bool HESS = false>
 __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, double h,
                                               double s_mid, int ib, int ie, Sums64 &out) {
   if (ie <= ib) return;
@@ -283,14 +305,12 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
   const double eG = exp_tab<true>(fmin(G * h, 709.0)), eGi = rcp64(eG);
   double qG = exp_tab<true>(m2v * tb);
   const double eq1 = exp_tab<true>(m2v * h), eqG = exp_tab<true>(m2v * (G * h));
-  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0;
   if (ib == 0) {
     // node 0 carries weight 1/2: take half of it back (exact state)
-    const double E = exp_tab<false>(fma(v, t0, -s_mid) - (XpG + XmG));
-    const double w = fma(E, qG, E);
-    S0 = -0.5 * w;
-    if (DX) S2 = -0.5 * (w * (XpG + XmG));
-    if (DV) S1 = -0.5 * (fma(E, 2.0, -w) * t0);
+    const double X = XpG + XmG;
+    const double E = exp_tab<false>(fma(v, t0, -s_mid) - X);
+    v2_accumulate<DV, DX, HESS>(-0.5 * E, qG, X, t0, S0, S1, S2, S11, S22, S12);
   }
   double md = (double)ib;
   int m = ib;
@@ -325,10 +345,8 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
-      const double w = fma(E, q[j], E);
-      S0 += w;
-      if (DX) S2 = fma(w, X[j], S2);
-      if (DV) S1 = fma(fma(E, 2.0, -w), j == 0 ? tc : fma(double(j), h, tc), S1);
+      v2_accumulate<DV, DX, HESS>(E, q[j], X[j], j == 0 ? tc : fma(double(j), h, tc), S0, S1,
+                                  S2, S11, S22, S12);
     }
   }
   double xp = XpG, xm = XmG, qq = qG;
@@ -337,15 +355,18 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
     const double t = fma((double)m, h, t0);
     const double X = xp + xm;
     const double E = exp_tab<false>(fma(v, t, -s_mid) - X);
-    const double w = fma(E, qq, E);
-    S0 += w;
-    if (DX) S2 = fma(w, X, S2);
-    if (DV) S1 = fma(fma(E, 2.0, -w), t, S1);
+    v2_accumulate<DV, DX, HESS>(E, qq, X, t, S0, S1, S2, S11, S22, S12);
     xp *= e1; xm *= e1i; qq *= eq1;
   }
+  const double rx = rcp64(x);
   out.S0 += S0;
-  if (DV) out.S1 += S1;
-  if (DX) out.S2 += S2 * rcp64(x);
+  if (DV || HESS) out.S1 += S1;
+  if (DX || HESS) out.S2 += S2 * rx;
+  if (HESS) {
+    out.S11 += S11;
+    out.S22 += (S22 * rx) * rx;
+    out.S12 += S12 * rx;
+  }
 }
 
 // Half of the last node's contributions, evaluated in FP32: that node sits
@@ -386,8 +407,8 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
   const double s_mid = shift + kLn2;                 // E = exp(vt - x cosh t - s_mid)
   (void)tab;
 #ifndef BLK_QUAD_V1
-  if (!HESS && !CLAMP && !(v > 0.0 && v * fma((double)n, h, t0) < 1e-3))
-    nodes_fp64_v2<DV, DX>(v, x, t0, h, s_mid, mb, me, s);
+  if (!CLAMP && !(v > 0.0 && v * fma((double)n, h, t0) < 1e-3))
+    nodes_fp64_v2<DV, DX, HESS>(v, x, t0, h, s_mid, mb, me, s);
   else
 #endif
     nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, s);
