@@ -7,24 +7,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _timing import device_time  # noqa: E402
+
 import paper_2108_11560_b200 as blk  # noqa: E402
 import workloads  # noqa: E402
 
 
+
 def timeit(fn, reps=20):
-    for _ in range(3):
-        fn()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        fn()
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ts.sort()
-    return ts[len(ts) // 2]
+    return device_time(fn, reps)
 
 
 def main():
@@ -50,10 +42,14 @@ def main():
     s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     P = [ctypes.c_void_p(t.data_ptr()) for t in (vt, xt, *o, scratch)]
     split = "--split" in os.environ.get("TS_OPTS", "")
+    lanes_list = [int(a) for a in os.environ.get("TS_LANES", "0").split(",")]
     for n in sizes:
-        ms = timeit(lambda: blk.bessel_logk_f64(vt[:n], xt[:n], o[0][:n], o[1][:n], o[2][:n], nbins=128))
-        line = f"{cfg} n={n:9d} waves={n / (6 * 148 * 128):6.2f} fused {ms:.4f} ms  {n / ms * 1e3:.3e} evals/s"
-        if split:
+      for lanes in lanes_list:
+        ms = timeit(lambda: blk.bessel_logk_f64(vt[:n], xt[:n], o[0][:n], o[1][:n], o[2][:n], nbins=128,
+                                                lanes_per_element=lanes))
+        line = (f"{cfg} n={n:9d} waves={n / (6 * 148 * 128):6.2f} lanes={lanes} fused {ms:.4f} ms  "
+                f"{n / ms * 1e3:.3e} evals/s")
+        if split and lanes == lanes_list[0]:
             f(P[0], P[1], n, P[2], P[3], P[4], 128, P[5], 1, s)
             mp = timeit(lambda: f(P[0], P[1], n, P[2], P[3], P[4], 128, P[5], 1, s))
             mq = timeit(lambda: f(P[0], P[1], n, P[2], P[3], P[4], 128, P[5], 2, s))
