@@ -122,56 +122,104 @@ def oracle_rate(cfg, nbins, seconds, threads):
 
 
 class ClockSampler:
+    """SM clock + clock-event reasons sampled DURING the timed region.
+
+    NVML (pynvml) polled from a thread every ~1 ms (the timed region of a
+    default run is only a few ms long, below nvidia-smi's 100 ms sampling);
+    only samples taken between mark_begin() and mark_end() count.  Falls back
+    to `nvidia-smi -lms 100` when NVML is unavailable."""
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
+        self.samples = []          # (t, sm_mhz, max_mhz, reasons_mask)
+        self.begin = self.end = None
+        self.stop_flag = threading.Event()
+        self.nvml = None
         self.proc = None
-        self.lines = []
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll_nvml, daemon=True)
+        except Exception:  # pragma: no cover - no NVML
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.thread = threading.Thread(target=self._read_smi, daemon=True)
+            except OSError:
+                return
+        self.thread.start()
 
-    def _read(self):
+    def _poll_nvml(self):
+        pynvml, h = self.nvml
+        while not self.stop_flag.is_set():
+            try:
+                mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:  # pragma: no cover
+                break
+            self.samples.append((time.perf_counter(), float(mhz), float(self.max_mhz), int(rs)))
+            time.sleep(0.001)
+
+    def _read_smi(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.thread.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
             f = [c.strip() for c in ln.split(",")]
             if len(f) < 8:
                 continue
             try:
-                sm.append(float(f[0]))
-                smax.append(float(f[1]))
+                mask = 0
+                for (nm, bit), val in zip((("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+                                           ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4)),
+                                          f[4:8]):
+                    if val.lower() == "active":
+                        mask |= bit
+                self.samples.append((time.perf_counter(), float(f[0]), float(f[1]), mask))
             except ValueError:
                 continue
-            for nm, val in zip(names, f[4:8]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+
+    def mark_begin(self):
+        self.begin = time.perf_counter()
+
+    def mark_end(self):
+        self.end = time.perf_counter()
+
+    def stop(self):
+        self.stop_flag.set()
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if getattr(self, "thread", None) is not None:
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"]}
+        lo = self.begin if self.begin is not None else -1e30
+        hi = self.end if self.end is not None else 1e30
+        inside = [smp for smp in self.samples if lo <= smp[0] <= hi] or self.samples
+        mask = 0
+        for smp in inside:
+            mask |= smp[3]
+        return {"sm_mhz": statistics.median(smp[1] for smp in inside),
+                "sm_max_mhz": max(smp[2] for smp in inside),
+                "samples": len(inside),
+                "source": "nvml 1 ms" if self.nvml else "nvidia-smi 100 ms",
+                "window": "timed region" if len(inside) < len(self.samples) or self.begin else "run",
+                "reasons": sorted(nm for nm, bit in self.REASONS if mask & bit)}
 
 
 def run_reference(args, rank, world):
@@ -278,12 +326,14 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    sampler.mark_begin()
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         starts[i].record(stream)
         step()
         ends[i].record(stream)
     torch.cuda.synchronize()
+    sampler.mark_end()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
