@@ -359,7 +359,13 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
   const size_t total = n * (size_t)lanes;
   const size_t blocks = (total + threads - 1) / threads;
   if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "grid too large");
+#ifdef BLK_SMEM_PAD
+  // tuning builds only: pad dynamic shared memory to cap resident blocks per SM
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BLK_SMEM_PAD);
+  kern<<<(unsigned)blocks, threads, BLK_SMEM_PAD, st>>>(v, x, n, a, b, c, nbins, mode);
+#else
   kern<<<(unsigned)blocks, threads, 0, st>>>(v, x, n, a, b, c, nbins, mode);
+#endif
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return BLK_OK;
