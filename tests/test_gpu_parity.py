@@ -351,3 +351,48 @@ def test_f32_fixed_point_exponent_edges():
     ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
     assert_parity(got, ref, "f32", "f32 edges")
     assert np.all(got["dv"][v == 0] == 0.0)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_wide_domain_fuzz(seed):
+    """Seeded fuzz far beyond the five configs (R22): v in {0} U logU[1e-6, 2e4],
+    x in logU[1e-12, 1e7], both range finders (FP32 for x in [1e-30, 1e4],
+    v <= 1e4; FP64 otherwise) and both quadrature loops.  Tolerance as in
+    test_extreme_domain: the north_star bounds, widened for the derivatives by
+    the exponent's own rounding eps*(x + v t_p) that the oracle also carries."""
+    rng = np.random.default_rng(seed)
+    n = 20000
+    v = 10.0 ** rng.uniform(-6, np.log10(2e4), n)
+    v[rng.random(n) < 0.02] = 0.0
+    v *= np.where(rng.random(n) < 0.1, -1.0, 1.0)
+    x = 10.0 ** rng.uniform(-12, 7, n)
+    got = run_gpu(v, x)
+    lk, dv, dx, plan = oracle.logk(v, x, NB, with_plan=True, threads=8)
+    from parity import errors
+    kappa = np.finfo(float).eps * (x + np.abs(v) * plan[:, 0] + 40.0)
+    tol_d = np.maximum(1e-10, 10 * kappa)
+    assert np.array_equal(np.isnan(got["logk"]), np.isnan(lk))
+    ok = ~np.isnan(lk)
+    e0 = errors(got["logk"][ok], lk[ok], "logk")
+    assert e0.max() <= 1e-12, (e0.max(), v[ok][np.argmax(e0)], x[ok][np.argmax(e0)])
+    e2 = errors(got["dx"][ok], dx[ok], "dx")
+    assert np.all(e2 <= tol_d[ok]), (v[ok][np.argmax(e2 / tol_d[ok])], x[ok][np.argmax(e2 / tol_d[ok])])
+    e1 = errors(got["dv"][ok], dv[ok], "dv")
+    assert np.all(e1 <= tol_d[ok]), (v[ok][np.argmax(e1 / tol_d[ok])], x[ok][np.argmax(e1 / tol_d[ok])])
+    assert np.all(got["dv"][v == 0] == 0.0)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_wide_domain_fuzz_f32(seed):
+    """FP32 entry point on a domain wider than config 4: v in {0} U U[0, 200],
+    x in logU[1e-4, 1e3]; FP32 tolerances against the FP64 oracle on the
+    widened float inputs."""
+    rng = np.random.default_rng(100 + seed)
+    n = 20000
+    v = rng.uniform(0.0, 200.0, n).astype(np.float32)
+    v[rng.random(n) < 0.02] = 0.0
+    x = (10.0 ** rng.uniform(-4, 3, n)).astype(np.float32)
+    got = run_gpu(v, x)
+    ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
+    assert_parity(got, ref, "f32", "f32 fuzz")
+    assert np.all(got["dv"][v == 0] == 0.0)
