@@ -454,7 +454,10 @@ blk_status run(const T *v, const T *x, size_t n, T *a, T *b, T *c, int nbins,
 }
 
 // ---- host-buffer pipeline
-constexpr int kHostStreams = 3;
+#ifndef BLK_HOST_STREAMS
+#define BLK_HOST_STREAMS 3
+#endif
+constexpr int kHostStreams = BLK_HOST_STREAMS;
 std::mutex g_pool_mu;
 struct Pool {
   int device = -1;
