@@ -16,6 +16,12 @@ ncu --set full --clock-control none --import-source on -k regex:logk_f64_kernel 
 echo "ncu rc=$?" >> gpurun_out/${TAG}_ncu_full.log
 CMD4="python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 ncu --set full --clock-control none --import-source on -k regex:logk_f32_kernel -s 3 -c 1 -o gpurun_out/${TAG}_prof_c4 $CMD4 > gpurun_out/${TAG}_ncu_full_c4.log 2>&1
+# keep gpurun_out small (<64 MiB merge limit): summaries + compressed source pages, drop the c4 report
+python tools/ncu_summary.py gpurun_out/${TAG}_prof.ncu-rep 1048576 gpurun_out/${TAG}_ncu_full_summary.txt > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/${TAG}_prof_c4.ncu-rep 67108864 gpurun_out/${TAG}_c4_ncu_full_summary.txt > /dev/null 2>&1
+ncu -i gpurun_out/${TAG}_prof.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/${TAG}_src.csv.gz
+ncu -i gpurun_out/${TAG}_prof_c4.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/${TAG}_src_c4.csv.gz
+rm -f gpurun_out/${TAG}_prof_c4.ncu-rep
 timeout 1200 python tools/report_configs.py --out gpurun_out/${TAG}_configs.json > gpurun_out/${TAG}_configs.log 2>&1
 timeout 1200 python tools/report_configs.py --nbins 64 --out gpurun_out/${TAG}_configs_n64.json > gpurun_out/${TAG}_configs_n64.log 2>&1
-tail -1 gpurun_out/${TAG}_smoke.log; tail -2 gpurun_out/${TAG}_pytest_gpu.log; cut -c1-200 gpurun_out/${TAG}_bench.log gpurun_out/${TAG}_bench_c4.log gpurun_out/${TAG}_bench_ref.log
+du -sh gpurun_out; tail -1 gpurun_out/${TAG}_smoke.log; tail -2 gpurun_out/${TAG}_pytest_gpu.log; cut -c1-200 gpurun_out/${TAG}_bench.log gpurun_out/${TAG}_bench_c4.log gpurun_out/${TAG}_bench_ref.log
