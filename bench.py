@@ -42,6 +42,10 @@ import workloads  # noqa: E402
 # launch / n) on config c2 at nbins=128 -- profiles/r01_p3_ncu_full_summary.txt,
 # DESIGN.md §5.  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
 FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4063.0}
+# FP32 entry point (c4, nbins=128), same method on the FP32 kernel
+# (profiles/s2f_c4_ncu_full_summary.txt, SASS per-op counts): FP32 flops (FFMA=2,
+# FFMA2=4), the FP64 flops of its exponent formation and MUFU ops per element.
+FP32_WORK_PER_ELEMENT = {("c4", 128): {"fp32_flops": 2713.4, "fp64_flops": 1217.0, "mufu": 275.4}}
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch (same capture),
 # per element; the outputs stay in L2 until after the kernel.
 DRAM_BYTES_PER_ELEMENT = {("c2", 128): 16.09}
@@ -402,8 +406,19 @@ def main():
                 "flops_per_element": flops_pe,
                 "hbm_gbs": (n * (16 + 8 * len(c.outputs))) / (ms_per_step * 1e-3) / 1e9}
     else:
-        roof = {"bound": "alu", "pipe": "fp32+mufu", "achieved": None,
-                "peak": fp32_ops * 2 / 1e12, "unit": "TFLOP/s", "frac": None, "traffic": None}
+        wk = FP32_WORK_PER_ELEMENT.get((args.config, args.nbins))
+        rate = n / (ms_per_step * 1e-3)
+        ach = wk["fp32_flops"] * rate / 1e12 if wk else None
+        peak32 = fp32_ops * 2 / 1e12
+        roof = {"bound": "alu", "pipe": "fp32 (with fp64 exponent and MUFU)", "achieved": ach,
+                "peak": peak32, "unit": "TFLOP/s", "frac": (ach / peak32) if ach else None,
+                "traffic": None,
+                "fp64_tflops": wk["fp64_flops"] * rate / 1e12 if wk else None,
+                "fp64_frac": (wk["fp64_flops"] * rate / 1e12) / (fp64_ops * 2 / 1e12) if wk else None,
+                "mufu_frac": (wk["mufu"] * rate) / mufu_ops if wk else None,
+                "peak_source": "in-run FFMA/DFMA/MUFU.EX2 microbenchmarks; the kernel is bound by "
+                               "register-file reads across the three pipes (DESIGN.md §5)",
+                "hbm_gbs": (n * 20) / (ms_per_step * 1e-3) / 1e9}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
