@@ -192,11 +192,13 @@ using PlanF32 = PlanF32T<false>;
 // which changes no output beyond rounding (R4, R20).  The literal
 // tol = 1 on |a_i - a_{i-1}| is not used (R4: it stops on the first
 // iteration that keeps a, and breaks config 3).
-// The tolerance follows the grid: with nbins >= 32 the trapezoid error is at
-// rounding level and insensitive to the range (R20), so 2^-10; coarser grids
-// are sensitive to where the nodes fall, so 2^-20 (FP32 resolution).
+// The tolerance follows the grid: from nbins = 64 the trapezoid error is at
+// rounding level and insensitive to the range (R20), so 2^-8 (the range is
+// then at most ~0.4% wider than converged); 32-63 bins still carry a
+// discretisation error that a wider range shifts, so 2^-10; coarser grids are
+// sensitive to where the nodes fall, so 2^-20 (FP32 resolution).
 __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
-  return nbins >= 32 ? 9.765625e-4f : 9.5367431640625e-7f;
+  return nbins >= 64 ? 3.90625e-3f : (nbins >= 32 ? 9.765625e-4f : 9.5367431640625e-7f);
 }
 template <bool PEAK, bool ASC, class PF>
 __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
@@ -205,10 +207,24 @@ __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, fl
   for (int i = 0; i < kMaxIter; ++i) {
     // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
     // carries no information and must not end the search)
+#ifdef BLK_FZ_EXIT_NEWTON
+    // same test on the Newton correction computed for the step anyway:
+    // |F(a)/F'(a)| <= tol |a|; rcp(F'(a)) = 0 for an overflowed F'(a), so
+    // the step is 0 there and the finiteness of F'(a) is checked explicitly
+    float mid, tn;
+    const float step = Fa * rcp_approx(dFa);
+    if (fabsf(step) <= tol * fabsf(a) && fabsf(dFa) <= 3.0e38f) break;
+    mid = fmaf(b - a, 0.5f, a);
+    {
+      const float t = a - step;
+      tn = ASC ? fmaxf(fminf(t, mid), a) : fminf(fmaxf(t, mid), a);
+    }
+#else
     const float rhs = tol * fabsf(a * dFa);
     if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
     float mid, tn;
     fz_points_f32<ASC>(a, Fa, dFa, b, mid, tn);
+#endif
     float2 F, dF;
     if (PEAK) P.peak2(f2(mid, tn), F, dF);
     else P.thr2(c, f2(mid, tn), F, dF);
