@@ -7,8 +7,9 @@
  *   For every element i the library finds the peak t_p of
  *   g(t) = log cosh(vt) - x cosh t (t_p = 0 when v^2 <= x,
  *   P:103-110) and the range [t0, t1] where g >= g(t_p) + log eps
- *    with Alg. 1 FindRange and Alg. 2 FindZero (fixed
- *   10 iterations), then integrates with a FIXED number of trapezoid
+ *    with Alg. 1 FindRange and Alg. 2 FindZero (at most
+ *   10 iterations, ending on the paper's "until" clause with a working
+ *   tolerance, R4), then integrates with a FIXED number of trapezoid
  *   intervals n = nbins (Eq. (int)) in log-sum-exp form:
  *     logk[i]     = log K_v(x)
  *     dlogk_dv[i] = d log K_v(x) / dv   (integrand t sinh(vt) e^{-x cosh t})
@@ -29,8 +30,10 @@
  *     negated (K is even in v).  The FindRange doubling cap (t <= t_s + 2^12)
  *     exceeded -> NaN.
  *   - Results are a pure function of (v[i], x[i], nbins, entry point,
- *     options): bit-identical across runs, batch permutations, shard counts
- *     and output subsets.
+ *     options, lanes per element): bit-identical across runs, batch
+ *     permutations, shard counts and output subsets.  (lanes_per_element = 0
+ *     picks the lane count from n, which can change the last ulps; pass an
+ *     explicit value for n-independent bits.)
  *   - Reentrant and thread-safe; no global mutable state except the one-time
  *     lazily created helper streams of the *_host entry points.
  *
