@@ -43,9 +43,9 @@ import workloads  # noqa: E402
 # DESIGN.md §5.  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
 FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4067.0}
 # FP32 entry point (c4, nbins=128), same method on the FP32 kernel
-# (profiles/s2f_c4_ncu_full_summary.txt, SASS per-op counts): FP32 flops (FFMA=2,
+# (profiles/r01_c4pk_ncu_full_summary.txt, SASS per-op counts): FP32 flops (FFMA=2,
 # FFMA2=4), the FP64 flops of its exponent formation and MUFU ops per element.
-FP32_WORK_PER_ELEMENT = {("c4", 128): {"fp32_flops": 2713.4, "fp64_flops": 1217.0, "mufu": 275.4}}
+FP32_WORK_PER_ELEMENT = {("c4", 128): {"fp32_flops": 2739.2, "fp64_flops": 1197.0, "mufu": 266.9}}
 # dram__bytes_read.sum + dram__bytes_write.sum of one launch (same capture),
 # per element; the outputs stay in L2 until after the kernel.
 DRAM_BYTES_PER_ELEMENT = {("c2", 128): 16.09}
