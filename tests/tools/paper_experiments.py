@@ -11,14 +11,14 @@
     x = 10^(3r-1), sizes 10 .. 2^28; time per call (CUDA events, one launch
     each, inputs resident) -- flat until the GPU is filled, then linear.
 
-usage: python tools/paper_experiments.py [--out profiles/r01_paper_experiments.json]
+usage: python tests/tools/paper_experiments.py [--out profiles/r01_paper_experiments.json]
 """
 import argparse
 import json
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402

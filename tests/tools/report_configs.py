@@ -1,12 +1,12 @@
 """Throughput + sampled parity on every BASELINE.json config (one GPU).
-usage: python tools/report_configs.py [--nbins 128] [--out profiles/x.json]
+usage: python tests/tools/report_configs.py [--nbins 128] [--out profiles/x.json]
 Prints one line per (config, nbins, kernel variant)."""
 import argparse
 import json
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402

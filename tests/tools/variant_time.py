@@ -1,17 +1,17 @@
 """Time the public entry point of several library builds on one config and
 check them against the oracle on a sample.
-usage: python tools/variant_time.py CFG N lib1.so lib2.so ..."""
+usage: python tests/tools/variant_time.py CFG N lib1.so lib2.so ..."""
 import ctypes
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, 'tools'))
 from _timing import device_time  # noqa: E402
 
 import oracle  # noqa: E402

@@ -22,6 +22,6 @@ python tools/ncu_summary.py gpurun_out/${TAG}_prof_c4.ncu-rep 67108864 gpurun_ou
 ncu -i gpurun_out/${TAG}_prof.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/${TAG}_src.csv.gz
 ncu -i gpurun_out/${TAG}_prof_c4.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/${TAG}_src_c4.csv.gz
 rm -f gpurun_out/${TAG}_prof_c4.ncu-rep
-timeout 1200 python tools/report_configs.py --out gpurun_out/${TAG}_configs.json > gpurun_out/${TAG}_configs.log 2>&1
-timeout 1200 python tools/report_configs.py --nbins 64 --out gpurun_out/${TAG}_configs_n64.json > gpurun_out/${TAG}_configs_n64.log 2>&1
+timeout 1200 python tests/tools/report_configs.py --out gpurun_out/${TAG}_configs.json > gpurun_out/${TAG}_configs.log 2>&1
+timeout 1200 python tests/tools/report_configs.py --nbins 64 --out gpurun_out/${TAG}_configs_n64.json > gpurun_out/${TAG}_configs_n64.log 2>&1
 du -sh gpurun_out; tail -1 gpurun_out/${TAG}_smoke.log; tail -2 gpurun_out/${TAG}_pytest_gpu.log; cut -c1-200 gpurun_out/${TAG}_bench.log gpurun_out/${TAG}_bench_c4.log gpurun_out/${TAG}_bench_ref.log
