@@ -200,6 +200,14 @@ using PlanF32 = PlanF32T<false>;
 __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
   return nbins >= 64 ? 3.90625e-3f : (nbins >= 32 ? 9.765625e-4f : 9.5367431640625e-7f);
 }
+// For the PEAK search (F = g', F' = g'') what matters is not where t_p is
+// but how far g(a) lies below the maximum, because g(t_p) becomes the
+// log-sum-exp shift and the base of the eps threshold: Newton's estimate of
+// that gap is F(a)^2 / (2 |F'(a)|), and the search stops once it is below
+// kPeakGapTol (1/16 in log units).  A relative criterion on t_p would leave
+// gaps of |g''| (tol t_p)^2 / 2 -- over 100 in log units for x ~ 1e-30 and
+// v ~ 1e4 (t_p ~ 78), enough to push FP32 weights out of range.
+constexpr float kPeakGapTol = 0.0625f;
 template <bool PEAK, bool ASC, class PF>
 __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
                                                float dFa, float b, float tol) {
@@ -207,24 +215,16 @@ __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, fl
   for (int i = 0; i < kMaxIter; ++i) {
     // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
     // carries no information and must not end the search)
-#ifdef BLK_FZ_EXIT_NEWTON
-    // same test on the Newton correction computed for the step anyway:
-    // |F(a)/F'(a)| <= tol |a|; rcp(F'(a)) = 0 for an overflowed F'(a), so
-    // the step is 0 there and the finiteness of F'(a) is checked explicitly
-    float mid, tn;
-    const float step = Fa * rcp_approx(dFa);
-    if (fabsf(step) <= tol * fabsf(a) && fabsf(dFa) <= 3.0e38f) break;
-    mid = fmaf(b - a, 0.5f, a);
-    {
-      const float t = a - step;
-      tn = ASC ? fmaxf(fminf(t, mid), a) : fminf(fmaxf(t, mid), a);
+    if (PEAK && tol >= 1e-4f) {
+      // (on coarse grids, tol = 2^-20, the peak too is found to FP32
+      // resolution: there the nodes' placement matters, see fz_tol_for)
+      if (Fa * Fa <= (2.0f * kPeakGapTol) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
+    } else {
+      const float rhs = tol * fabsf(a * dFa);
+      if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
     }
-#else
-    const float rhs = tol * fabsf(a * dFa);
-    if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
     float mid, tn;
     fz_points_f32<ASC>(a, Fa, dFa, b, mid, tn);
-#endif
     float2 F, dF;
     if (PEAK) P.peak2(f2(mid, tn), F, dF);
     else P.thr2(c, f2(mid, tn), F, dF);

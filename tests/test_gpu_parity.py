@@ -282,7 +282,7 @@ def test_paper_accuracy_grid():
     import importlib.util
     import os
     spec = importlib.util.spec_from_file_location(
-        "paper_experiments", os.path.join(os.path.dirname(__file__), "..", "tools",
+        "paper_experiments", os.path.join(os.path.dirname(__file__), "tools",
                                           "paper_experiments.py"))
     pe = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(pe)
@@ -396,3 +396,15 @@ def test_wide_domain_fuzz_f32(seed):
     ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
     assert_parity(got, ref, "f32", "f32 fuzz")
     assert np.all(got["dv"][v == 0] == 0.0)
+
+
+def test_f32_extreme_peaks():
+    """FP32 entry point where the peak sits far out (t_p up to ~80) and g is
+    sharply curved there (|g''| ~ 1e3-1e4): the peak search must bound the
+    gap g(max) - g(t_p) (the log-sum-exp shift), not the position of t_p,
+    or the fixed-point FP32 weights overflow (R4)."""
+    v = np.array([1e4, 1e4, 5e3, 2e3, 1e4, 8e3, 300.0, 1e4], np.float32)
+    x = np.array([1e-30, 1e-25, 1e-20, 1e-30, 1e-10, 1e-3, 1e-30, 1.0], np.float32)
+    got = run_gpu(v, x)
+    ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
+    assert_parity(got, ref, "f32", "f32 extreme peaks")
