@@ -216,7 +216,7 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
-  Sums32 s{0.0f, 0.0f, 0.0f};
+  Sums32 s{0.0, 0.0, 0.0};
   const float h = (t1 - t0) / nbins;
   if (ok) {
     int mb, me;
@@ -237,9 +237,10 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   }
   if (!live || sub != 0) return;
   const float nanv = __int_as_float(0x7fc00000);
-  if (LOGK) logk[i] = ok ? gp + logf(h) + logf(s.S0) : nanv;
-  if (DV) dlogk_dv[i] = ok ? sgn * __fdiv_rn(s.S1, s.S0) : nanv;
-  if (DX) dlogk_dx[i] = ok ? -__fdiv_rn(s.S2, s.S0) : nanv;
+  const double r0 = rcp64(s.S0);
+  if (LOGK) logk[i] = ok ? gp + logf(h) + logf(float(s.S0)) : nanv;
+  if (DV) dlogk_dv[i] = ok ? sgn * float(s.S1 * r0) : nanv;
+  if (DX) dlogk_dx[i] = ok ? -float(s.S2 * r0) : nanv;
 }
 
 // ------------------------------------------------------------ microbenchmarks

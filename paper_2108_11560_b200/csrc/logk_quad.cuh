@@ -423,8 +423,10 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
 }
 
 // ---------------------------------------------------------------- FP32 path
+// FP32 entry point sums, returned in FP64: S2 (and S1) can exceed FLT_MAX
+// where their ratio to S0, the output, does not.
 struct Sums32 {
-  float S0, S1, S2;
+  double S0, S1, S2;
 };
 
 // exp(a) with the argument split so that ex2.approx sees an exactly
@@ -480,6 +482,8 @@ __device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float 
   const double v2 = v * kLog2e, nx2 = -x * kLog2e;
   const double ns2 = -((double)shift + kLn2) * kLog2e;
   const double eh = exp(h), ehi = rcp64(eh);
+  const int sig = max(0, (int)ceil(fma((double)n, h, t0) * kLog2e) - 64);
+  const double sc_sig = ldexp(1.0, sig), sc_inv = ldexp(1.0, -sig);
   const float ehf = float(eh), ehif = float(ehi);
   const float m2vl = float(-2.0 * v2);
   const float eqf = ex2_approx(m2vl * hf);
@@ -493,7 +497,7 @@ __device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float 
     double et = 0.5 * exp(tc), eti = 0.25 * rcp64(et);
     const float tcf = float(tc);
     // FP32 copies of t and e^{+-t}/2 for the products (weights only)
-    float etf = float(et), etif = float(eti);
+    float etf = float(et * sc_inv), etif = float(eti * sc_inv);   // 2^-sig scaled (see v2)
     float q = ex2_approx(m2vl * tcf);                      // q, p re-anchored per chunk
     float p = -expm1f(-2.0f * vf * tcf);
     float B0 = 0.0f, B1 = 0.0f, B2 = 0.0f;                 // per-chunk FP32 partial sums
@@ -548,7 +552,7 @@ __device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float 
       etf *= ehf;
       etif *= ehif;
     }
-    S0 += B0; S1 += B1; S2 += B2;
+    S0 += B0; S1 += B1; S2 += double(B2) * sc_sig;
   }
   // half weights of nodes 0 and n, evaluated directly
   auto half_node = [&](int mm) {
@@ -560,12 +564,12 @@ __device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float 
     const float q1 = ex2_approx(m2vl * tf);
     const float w = fmaf(E, q1, E);
     S0 -= w;
-    if (DX) S2 -= double(w) * float(ch);
+    if (DX) S2 -= double(w) * ch;
     if (DV) S1 -= double(E * tf) * (-expm1f(-2.0f * vf * tf));
   };
   if (mb == 0) half_node(0);
   if (me == n + 1) half_node(n);
-  return Sums32{float(S0), float(S1), float(S2)};
+  return Sums32{S0, S1, S2};
 }
 
 // FP32 entry point, fast path.  The weight exponent in log2 units,
@@ -612,6 +616,14 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
   const double tb = fma((double)mb, h, t0);
   const double ebx = exp(tb);
   double XpG = hx2 * ebx, XmG = hx2 * rcp64(ebx);
+  // The FP32 cosh state is kept scaled by 2^-sig so that e^t stays below 2^64
+  // up to t1, leaving room for weights up to ~2^30 in the FP32 sums (e^t
+  // overflows FP32 beyond t = 88.7, where |d log K/dx| ~ cosh t_p itself
+  // approaches FLT_MAX); sig = 0 whenever t1 < 44, i.e. on every config.
+  const int sig = max(0, (int)ceil(fma((double)n, h, t0) * kLog2e) - 64);
+  const double sc_sig = ldexp(1.0, sig);
+  const double sc_et = ldexp(0.5 / hx2, -sig);
+  const float k_eti = float(ldexp(0.25, -2 * sig));
   double S0 = 0.0, S1 = 0.0, S2 = 0.0;
   double md = (double)mb;
   int m = mb;
@@ -621,8 +633,8 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
     const double tcd = fma(md, h, t0);
     const float tcf = float(tcd);
     // FP32 state re-anchored per block: e^{+-t}/2, q = e^{-2vt}, p = 1 - q
-    float etf = float(XpG * (0.5 / hx2));                // e^t / 2, e^-t / 2 (FP32 state)
-    float etif = 0.25f * rcp_approx(etf);
+    float etf = float(XpG * sc_et);                      // 2^-sig e^{+-t} / 2 (FP32 state)
+    float etif = k_eti * rcp_approx(etf);
     float q = ex2_approx(m2vl * tcf);
     float p = -expm1f(-2.0f * vf * tcf);
     float tf = tcf;
@@ -681,7 +693,7 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
       etif *= ehif;
       tf += hf;
     }
-    S0 += B0; S1 += B1; S2 += B2;
+    S0 += B0; S1 += B1; S2 += double(B2) * sc_sig;
   }
   // half weights of nodes 0 and n, evaluated directly; X at
   // node 0 is the exact start state (mb == 0) and at node n = me - 1 one
@@ -698,7 +710,7 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
   };
   if (mb == 0) half_node(0, hx2 * (ebx + rcp64(ebx)));
   if (me == n + 1) half_node(n, fma(XpG, e1i, XmG * e1));
-  return Sums32{float(S0), float(S1), float(S2)};
+  return Sums32{S0, S1, S2};
 }
 
 }  // namespace blk

@@ -408,3 +408,30 @@ def test_f32_extreme_peaks():
     got = run_gpu(v, x)
     ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
     assert_parity(got, ref, "f32", "f32 extreme peaks")
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_wide_domain_fuzz_f32_full(seed):
+    """FP32 entry point over its whole range-finder domain and beyond:
+    v in {0} U logU[1e-4, 2e4], x in logU[1e-36, 1e6] (the FP32 range finder
+    for x in [1e-30, 1e4], v <= 1e4, the FP64 one elsewhere), FP32
+    tolerances against the FP64 oracle on the widened float inputs."""
+    rng = np.random.default_rng(200 + seed)
+    n = 20000
+    v = (10.0 ** rng.uniform(-4, np.log10(2e4), n)).astype(np.float32)
+    v[rng.random(n) < 0.02] = 0.0
+    x = (10.0 ** rng.uniform(-36, 6, n)).astype(np.float32)
+    got = run_gpu(v, x)
+    ref = run_oracle(v.astype(np.float64), x.astype(np.float64))
+    # where the exact output is beyond FLT_MAX (d log K/dx ~ -cosh t_p for
+    # t_p > 88.7), the FP32 result is the correctly signed infinity
+    big = {k: np.abs(r) > np.finfo(np.float32).max for k, r in ref.items()}
+    fmax = float(np.finfo(np.float32).max)
+    for k in ref:
+        g, r = got[k][big[k]].astype(np.float64), ref[k][big[k]]
+        # +-inf, or FLT_MAX itself when the exact value is within rounding of it
+        assert np.all((np.sign(g) == np.sign(r)) & (np.abs(g) >= fmax * (1 - 1e-4))), k
+    keep = ~(big["logk"] | big["dv"] | big["dx"])
+    assert keep.mean() > 0.95
+    assert_parity({k: g[keep] for k, g in got.items()}, {k: r[keep] for k, r in ref.items()},
+                  "f32", "f32 full-domain fuzz")
