@@ -435,3 +435,23 @@ def test_wide_domain_fuzz_f32_full(seed):
     assert keep.mean() > 0.95
     assert_parity({k: g[keep] for k, g in got.items()}, {k: r[keep] for k, r in ref.items()},
                   "f32", "f32 full-domain fuzz")
+
+
+def test_f64_far_out_extremes():
+    """FP64 ranges as far out as double allows: t_p up to ~700 (x down to
+    1e-300, where e^t_p is near DBL_MAX), orders up to 1e6; x = 1e-305 puts
+    t_p past 709, where the oracle's own cosh overflows and both sides must
+    return NaN.  Tolerances as in test_extreme_domain."""
+    v = np.array([1e4, 1e4, 1.0, 100.0, 1e4, 1e6, 1e5, 2.5, 0.0])
+    x = np.array([1e-305, 1e-300, 1e-300, 1e-250, 1e-200, 1.0, 1e-10, 1e-280, 1e-300])
+    got = run_gpu(v, x)
+    lk, dv, dx, plan = oracle.logk(v, x, NB, with_plan=True)
+    from parity import errors
+    for g, r in ((got["logk"], lk), (got["dv"], dv), (got["dx"], dx)):
+        assert np.array_equal(np.isnan(g), np.isnan(r))
+    ok = ~np.isnan(lk)
+    kappa = np.finfo(float).eps * (x + v * np.nan_to_num(plan[:, 0]) + 40.0)
+    tol_d = np.maximum(1e-10, 10 * kappa)
+    assert np.all(errors(got["logk"][ok], lk[ok], "logk") <= 1e-12)
+    assert np.all(errors(got["dx"][ok], dx[ok], "dx") <= tol_d[ok])
+    assert np.all(errors(got["dv"][ok], dv[ok], "dv") <= tol_d[ok])
