@@ -455,3 +455,25 @@ def test_f64_far_out_extremes():
     assert np.all(errors(got["logk"][ok], lk[ok], "logk") <= 1e-12)
     assert np.all(errors(got["dx"][ok], dx[ok], "dx") <= tol_d[ok])
     assert np.all(errors(got["dv"][ok], dv[ok], "dv") <= tol_d[ok])
+
+
+def test_hessian_wide_fuzz():
+    """Second derivatives beyond the configs: v in {0} U logU[1e-3, 1e3], x in
+    logU[1e-6, 1e4]; bound as in test_parity_hessian, widened by the
+    exponent's own rounding eps*(x + v t_p) that both sides carry."""
+    rng = np.random.default_rng(7)
+    n = 6000
+    v = 10.0 ** rng.uniform(-3, 3, n)
+    v[rng.random(n) < 0.03] = 0.0
+    x = 10.0 ** rng.uniform(-6, 4, n)
+    dev = torch.device("cuda")
+    out = blk.log_bessel_k_hess(torch.from_numpy(v).to(dev), torch.from_numpy(x).to(dev))
+    torch.cuda.synchronize()
+    got = [o.cpu().numpy() for o in out]
+    lk, dv, dx, dvv, dxx, dvx = oracle.logk_hess(v, x, NB, threads=8)
+    _, _, _, plan = oracle.logk(v, x, NB, with_plan=True, threads=8)
+    kap = np.maximum(1.0, 10 * np.finfo(float).eps * (x + v * plan[:, 0] + 40.0) / 1e-10)
+    for g, r, mom in ((got[3], dvv, np.abs(dvv) + dv * dv), (got[4], dxx, np.abs(dxx) + dx * dx),
+                      (got[5], dvx, np.abs(dvx) + np.abs(dv * dx))):
+        bad = np.abs(g - r) > kap * (1e-10 * np.abs(r) + 1e-12 * mom)
+        assert not bad.any(), (v[bad][:4], x[bad][:4], g[bad][:3], r[bad][:3])
