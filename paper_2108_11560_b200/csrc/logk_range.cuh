@@ -192,13 +192,14 @@ using PlanF32 = PlanF32T<false>;
 // which changes no output beyond rounding (R4, R20).  The literal
 // tol = 1 on |a_i - a_{i-1}| is not used (R4: it stops on the first
 // iteration that keeps a, and breaks config 3).
-// The tolerance follows the grid: from nbins = 64 the trapezoid error is at
+// The tolerance follows the grid: from nbins = 128 the trapezoid error is at
 // rounding level and insensitive to the range (R20), so 2^-8 (the range is
-// then at most ~0.4% wider than converged); 32-63 bins still carry a
-// discretisation error that a wider range shifts, so 2^-10; coarser grids are
-// sensitive to where the nodes fall, so 2^-20 (FP32 resolution).
+// then at most ~0.4% of its half-width wider than converged); 64-127 bins can
+// still carry a discretisation error on extreme inputs that a wider range
+// shifts, so 2^-10; coarser grids are sensitive to where the nodes fall, so
+// 2^-20 (FP32 resolution), and there the peak is found to that resolution too.
 __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
-  return nbins >= 64 ? 3.90625e-3f : (nbins >= 32 ? 9.765625e-4f : 9.5367431640625e-7f);
+  return nbins >= 128 ? 3.90625e-3f : (nbins >= 64 ? 9.765625e-4f : 9.5367431640625e-7f);
 }
 // For the PEAK search (F = g', F' = g'') what matters is not where t_p is
 // but how far g(a) lies below the maximum, because g(t_p) becomes the
@@ -208,19 +209,23 @@ __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
 // gaps of |g''| (tol t_p)^2 / 2 -- over 100 in log units for x ~ 1e-30 and
 // v ~ 1e4 (t_p ~ 78), enough to push FP32 weights out of range.
 constexpr float kPeakGapTol = 0.0625f;
+// For the range ends the Newton correction is measured against the distance
+// of a from the peak t_p (`ref`), the scale of the half-range, not against
+// |a|: for a far peak (t_p ~ 14 with a half-range of 0.3) |a| would allow
+// steps of several percent of the range.
 template <bool PEAK, bool ASC, class PF>
 __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
-                                               float dFa, float b, float tol) {
+                                               float dFa, float b, float tol, float ref = 0.0f) {
 #pragma unroll 2
   for (int i = 0; i < kMaxIter; ++i) {
     // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
     // carries no information and must not end the search)
-    if (PEAK && tol >= 1e-4f) {
+    if (PEAK && tol >= 3e-3f) {
       // (on coarse grids, tol = 2^-20, the peak too is found to FP32
       // resolution: there the nodes' placement matters, see fz_tol_for)
       if (Fa * Fa <= (2.0f * kPeakGapTol) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
     } else {
-      const float rhs = tol * fabsf(a * dFa);
+      const float rhs = tol * fabsf((a - ref) * dFa);
       if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
     }
     float mid, tn;
@@ -273,10 +278,10 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   const float c = p.gp + P.L + float(kLn2);
   p.t0 = 0.0f;
   float d0 = -P.x - p.gp - P.L;                                    // d(0)
-  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp, tol);
+  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp, tol, p.tp);
   auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
   if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
-  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol);
+  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol, p.tp);
   p.dmin = fminf(d0, Fh);
   p.ok = true;
   return p;

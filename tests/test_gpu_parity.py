@@ -477,3 +477,46 @@ def test_hessian_wide_fuzz():
                       (got[5], dvx, np.abs(dvx) + np.abs(dv * dx))):
         bad = np.abs(g - r) > kap * (1e-10 * np.abs(r) + 1e-12 * mom)
         assert not bad.any(), (v[bad][:4], x[bad][:4], g[bad][:3], r[bad][:3])
+
+
+def _wide_inputs(seed, n=6000):
+    rng = np.random.default_rng(seed)
+    v = 10.0 ** rng.uniform(-6, 4, n)
+    v[rng.random(n) < 0.02] = 0.0
+    x = 10.0 ** rng.uniform(-12, 6, n)
+    return v, x
+
+
+def _assert_wide(got, v, x, nbins):
+    lk, dv, dx, plan = oracle.logk(v, x, nbins, with_plan=True, threads=8)
+    from parity import errors
+    kappa = np.finfo(float).eps * (x + np.abs(v) * plan[:, 0] + 40.0)
+    tol_d = np.maximum(1e-10, 10 * kappa)
+    ok = ~np.isnan(lk)
+    assert np.array_equal(np.isnan(got["logk"]), ~ok)
+    assert errors(got["logk"][ok], lk[ok], "logk").max() <= 1e-12
+    assert np.all(errors(got["dx"][ok], dx[ok], "dx") <= tol_d[ok])
+    assert np.all(errors(got["dv"][ok], dv[ok], "dv") <= tol_d[ok])
+
+
+@pytest.mark.parametrize("lanes,kernel,nbins", [(2, 0, 128), (8, 0, 128), (32, 0, 200), (1, 2, 128),
+                                                (4, 0, 160), (1, 0, 2048)])
+def test_wide_domain_fuzz_variants(lanes, kernel, nbins):
+    """The wide-domain FP64 fuzz through the other launch variants (lanes per
+    element, the warp-specialised kernel, other converged bin counts)."""
+    v, x = _wide_inputs(lanes * 1000 + kernel * 10 + nbins)
+    _assert_wide(run_gpu(v, x, nbins=nbins, lanes_per_element=lanes, kernel=kernel), v, x, nbins)
+
+
+@pytest.mark.parametrize("lanes,nbins", [(8, 64), (4, 33), (1, 48)])
+def test_wide_domain_coarse_bins_f64_range(lanes, nbins):
+    """Coarse grids on the wide domain: small v with x ~ 1e-10 puts t_p ~ 25
+    and the range ~30 wide, so 16-64 nodes leave discretisation errors up to
+    ~1e-4 -- any conservative range is then equally correct (R20) but gives a
+    different error, and the FP32 range finder's range differs from the
+    oracle's.  The FP64 range finder (the paper's working precision,
+    BLK_RANGE_F64) reproduces the oracle's ranges and therefore its values to
+    the FP64 tolerance."""
+    v, x = _wide_inputs(4242 + nbins)
+    _assert_wide(run_gpu(v, x, nbins=nbins, lanes_per_element=lanes,
+                         range_mode=blk.BLK_RANGE_F64), v, x, nbins)
