@@ -39,9 +39,9 @@ import workloads  # noqa: E402
 # Per-element FP64 work of the fused kernel's algorithm (DFMA counted as 2
 # flops, DADD/DMUL as 1): the FP64 operations the kernel executes per element
 # (ncu sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on over one
-# launch / n) on config c2 at nbins=128 -- profiles/r01s2f_ncu_full_summary.txt,
+# launch / n) on config c2 at nbins=128 -- profiles/r01s2g_ncu_full_summary.txt,
 # DESIGN.md §5.  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
-FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4067.0}
+FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4056.0}
 # FP32 entry point (c4, nbins=128), same method on the FP32 kernel
 # (profiles/r01_c4pk_ncu_full_summary.txt, SASS per-op counts): FP32 flops (FFMA=2,
 # FFMA2=4), the FP64 flops of its exponent formation and MUFU ops per element.
