@@ -4,7 +4,7 @@
 // (SURVEY.md §8(a) a1-a7): load + canonicalise, regime test, peak, t0, t1
 // (logk_range.cuh), fixed-bin quadrature with the three sums
 // (logk_quad.cuh), epilogue log/divide, store.  No shared state besides the
-// 2 KB exp table per block; no atomics.  LPE (lanes per element) > 1 splits
+// 16 KB exp table per block of the FP64 kernels; no atomics.  LPE (lanes per element) > 1 splits
 // the n+1 nodes of one element across LPE adjacent lanes (every lane derives
 // the identical plan) and combines the sums with warp shuffles.
 #include <cuda_runtime.h>
