@@ -94,3 +94,17 @@ def test_no_oracle_in_product_path():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt and "oracle.c" not in txt, f
+
+
+def test_oracle_used_only_where_allowed():
+    """oracle/ is test infrastructure: only tests/, __graft_entry__.py (smoke)
+    and bench.py (cpu_baseline / --impl reference) may import it."""
+    allowed = {os.path.join(ROOT, "__graft_entry__.py"), os.path.join(ROOT, "bench.py")}
+    skip = {os.path.join(ROOT, d) for d in ("tests", "oracle", ".git", "gpurun_out", "baseline")}
+    for dp, dirs, files in os.walk(ROOT):
+        dirs[:] = [d for d in dirs if os.path.join(dp, d) not in skip]
+        for f in files:
+            path = os.path.join(dp, f)
+            if f.endswith(".py") and path not in allowed:
+                txt = open(path).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, path
