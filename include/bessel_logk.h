@@ -140,6 +140,12 @@ BLK_API blk_status bessel_logk_f64_host(const double *v, const double *x, size_t
                                 double *logk, double *dlogk_dv, double *dlogk_dx,
                                 int nbins, void *workspace, size_t workspace_bytes,
                                 size_t chunk, cudaStream_t stream);
+/* The same for the FP32 entry point: float host arrays; workspace of at
+ * least bessel_logk_host_workspace_bytes(chunk, 4) bytes. */
+BLK_API blk_status bessel_logk_f32_host(const float *v, const float *x, size_t n,
+                                float *logk, float *dlogk_dv, float *dlogk_dx,
+                                int nbins, void *workspace, size_t workspace_bytes,
+                                size_t chunk, cudaStream_t stream);
 
 /*
  * Diagnostic entry point: the FP64 hot path as two kernels -- `phases` bit 0

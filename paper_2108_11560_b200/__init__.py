@@ -23,6 +23,7 @@ __all__ = [
     "BLK_KERNEL_AUTO", "BLK_KERNEL_SIMPLE", "BLK_KERNEL_WS",
     "BesselLogKError", "lib", "library_path", "header_functions",
     "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
+    "bessel_logk_f32_host",
     "host_workspace_bytes", "microbench", "DEFAULT_NBINS", "nig_loglik", "log_bessel_k_hess",
 ]
 
@@ -74,8 +75,10 @@ def lib():
             f.argtypes = [vp, vp, sz, vp, vp, vp, ci, ctypes.POINTER(_Options), vp]
         L.bessel_logk_host_workspace_bytes.restype = sz
         L.bessel_logk_host_workspace_bytes.argtypes = [sz, sz]
-        L.bessel_logk_f64_host.restype = ci
-        L.bessel_logk_f64_host.argtypes = [vp, vp, sz, vp, vp, vp, ci, vp, sz, sz, vp]
+        for name in ("bessel_logk_f64_host", "bessel_logk_f32_host"):
+            f = getattr(L, name)
+            f.restype = ci
+            f.argtypes = [vp, vp, sz, vp, vp, vp, ci, vp, sz, sz, vp]
         L.bessel_logk_last_error.restype = ctypes.c_char_p
         L.bessel_logk_version.restype = ctypes.c_char_p
         L.bessel_logk_hess_f64.restype = ci
@@ -183,26 +186,38 @@ def host_workspace_bytes(chunk=0, elem_bytes=8):
     return lib().bessel_logk_host_workspace_bytes(int(chunk), int(elem_bytes))
 
 
-def bessel_logk_f64_host(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
-                         workspace=None, chunk=0, stream=None):
-    """Host-buffer entry point: v, x, outputs are CPU float64 tensors (pinned for overlap);
-    ``workspace`` a CUDA uint8 tensor of >= host_workspace_bytes(chunk) bytes."""
+def _host_call(prec, v, x, logk, dlogk_dv, dlogk_dx, nbins, workspace, chunk, stream):
     import torch
+    dtype = torch.float64 if prec == 64 else torch.float32
     n = v.numel()
 
     def hp(t, name):
         if t is None:
             return None
-        if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != n:
-            raise TypeError(f"{name} must be a contiguous CPU float64 tensor of {n} elements")
+        if t.is_cuda or t.dtype != dtype or not t.is_contiguous() or t.numel() != n:
+            raise TypeError(f"{name} must be a contiguous CPU {dtype} tensor of {n} elements")
         return ctypes.c_void_p(t.data_ptr())
 
     if workspace is None or not workspace.is_cuda:
         raise TypeError("workspace must be a CUDA tensor")
-    _check(lib().bessel_logk_f64_host(
-        hp(v, "v"), hp(x, "x"), n, hp(logk, "logk"), hp(dlogk_dv, "dlogk_dv"),
-        hp(dlogk_dx, "dlogk_dx"), int(nbins), ctypes.c_void_p(workspace.data_ptr()),
-        workspace.numel() * workspace.element_size(), int(chunk), _stream_handle(stream)))
+    f = lib().bessel_logk_f64_host if prec == 64 else lib().bessel_logk_f32_host
+    _check(f(hp(v, "v"), hp(x, "x"), n, hp(logk, "logk"), hp(dlogk_dv, "dlogk_dv"),
+             hp(dlogk_dx, "dlogk_dx"), int(nbins), ctypes.c_void_p(workspace.data_ptr()),
+             workspace.numel() * workspace.element_size(), int(chunk), _stream_handle(stream)))
+
+
+def bessel_logk_f64_host(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
+                         workspace=None, chunk=0, stream=None):
+    """Host-buffer entry point: v, x, outputs are CPU float64 tensors (pinned for overlap);
+    ``workspace`` a CUDA uint8 tensor of >= host_workspace_bytes(chunk) bytes."""
+    _host_call(64, v, x, logk, dlogk_dv, dlogk_dx, nbins, workspace, chunk, stream)
+
+
+def bessel_logk_f32_host(v, x, logk=None, dlogk_dv=None, dlogk_dx=None, nbins=DEFAULT_NBINS,
+                         workspace=None, chunk=0, stream=None):
+    """FP32 host-buffer entry point: CPU float32 tensors; ``workspace`` of >=
+    host_workspace_bytes(chunk, 4) bytes."""
+    _host_call(32, v, x, logk, dlogk_dv, dlogk_dx, nbins, workspace, chunk, stream)
 
 
 def microbench(kind, blocks, threads, iters, out, stream=None):

@@ -520,20 +520,25 @@ size_t bessel_logk_host_workspace_bytes(size_t chunk, size_t elem_bytes) {
   return (size_t)kHostStreams * 5 * arr;
 }
 
-blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, double *logk,
-                                double *dlogk_dv, double *dlogk_dx, int nbins, void *workspace,
-                                size_t workspace_bytes, size_t chunk, cudaStream_t stream) {
+}  // extern "C"
+
+namespace {
+// H2D -> kernel -> D2H pipeline over chunks on the helper streams (both precisions).
+template <class T>
+blk_status run_host(const T *v, const T *x, size_t n, T *logk, T *dlogk_dv, T *dlogk_dx,
+                    int nbins, void *workspace, size_t workspace_bytes, size_t chunk,
+                    cudaStream_t stream) {
   int lanes, mode, th, kernel;
   blk_status st = validate(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, nullptr, lanes, mode, th, kernel);
   if (st != BLK_OK) return st;
   if (n == 0) return BLK_OK;
   if (chunk == 0) chunk = (size_t)1 << 20;
-  if (!workspace || workspace_bytes < bessel_logk_host_workspace_bytes(chunk, 8))
+  if (!workspace || workspace_bytes < bessel_logk_host_workspace_bytes(chunk, sizeof(T)))
     return fail(BLK_EINVAL, "workspace missing or too small");
   Pool *pool;
   st = get_pool(pool);
   if (st != BLK_OK) return st;
-  const size_t arr = ((chunk * 8) + 255) / 256 * 256;
+  const size_t arr = ((chunk * sizeof(T)) + 255) / 256 * 256;
   cudaError_t e;
   // order after the caller's prior work
   cudaEvent_t start_ev;
@@ -546,11 +551,10 @@ blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, doub
     const int k = (int)(c % kHostStreams);
     cudaStream_t s = pool->s[k];
     char *base = (char *)workspace + (size_t)k * 5 * arr;
-    double *dv_ = (double *)(base), *dx_ = (double *)(base + arr);
-    double *o0 = (double *)(base + 2 * arr), *o1 = (double *)(base + 3 * arr),
-           *o2 = (double *)(base + 4 * arr);
+    T *dv_ = (T *)(base), *dx_ = (T *)(base + arr);
+    T *o0 = (T *)(base + 2 * arr), *o1 = (T *)(base + 3 * arr), *o2 = (T *)(base + 4 * arr);
     const size_t off = c * chunk, m = (n - off < chunk) ? n - off : chunk;
-    const size_t bytes = m * 8;
+    const size_t bytes = m * sizeof(T);
     if ((e = cudaMemcpyAsync(dv_, v + off, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
       return cuda_fail(e, "H2D v");
     if ((e = cudaMemcpyAsync(dx_, x + off, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -558,8 +562,8 @@ blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, doub
     // one element per lane in every chunk: results do not depend on the
     // chunking and equal a device-path call with lanes_per_element = 1
     blk_options o{1, mode, th, BLK_KERNEL_SIMPLE};
-    st = run<double>(dv_, dx_, m, logk ? o0 : nullptr, dlogk_dv ? o1 : nullptr,
-                     dlogk_dx ? o2 : nullptr, nbins, &o, s);
+    st = run<T>(dv_, dx_, m, logk ? o0 : nullptr, dlogk_dv ? o1 : nullptr,
+                dlogk_dx ? o2 : nullptr, nbins, &o, s);
     if (st != BLK_OK) return st;
     if (logk && (e = cudaMemcpyAsync(logk + off, o0, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
       return cuda_fail(e, "D2H logk");
@@ -575,6 +579,22 @@ blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, doub
   cudaEventDestroy(start_ev);
   if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "synchronize");
   return BLK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n, double *logk,
+                                double *dlogk_dv, double *dlogk_dx, int nbins, void *workspace,
+                                size_t workspace_bytes, size_t chunk, cudaStream_t stream) {
+  return run_host<double>(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, workspace, workspace_bytes,
+                          chunk, stream);
+}
+blk_status bessel_logk_f32_host(const float *v, const float *x, size_t n, float *logk,
+                                float *dlogk_dv, float *dlogk_dx, int nbins, void *workspace,
+                                size_t workspace_bytes, size_t chunk, cudaStream_t stream) {
+  return run_host<float>(v, x, n, logk, dlogk_dv, dlogk_dx, nbins, workspace, workspace_bytes,
+                         chunk, stream);
 }
 
 size_t bessel_nig_workspace_bytes(size_t n) {

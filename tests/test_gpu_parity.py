@@ -205,6 +205,19 @@ def test_host_entry_point_matches_device_path():
         assert np.array_equal(o.numpy(), dev[k]), k
 
 
+def test_host_entry_point_f32_matches_device_path():
+    v, x = workloads.generate("c4", 0, 50003)
+    dev = run_gpu(v, x, lanes_per_element=1)
+    vt = torch.from_numpy(v).pin_memory()
+    xt = torch.from_numpy(x).pin_memory()
+    outs = [torch.empty(v.size, dtype=torch.float32).pin_memory() for _ in range(3)]
+    chunk = 8192
+    ws = torch.empty(blk.host_workspace_bytes(chunk, 4), dtype=torch.uint8, device=DEV)
+    blk.bessel_logk_f32_host(vt, xt, *outs, nbins=NB, workspace=ws, chunk=chunk)
+    for k, o in zip(KINDS, outs):
+        assert np.array_equal(o.numpy(), dev[k]), k
+
+
 def test_mathematical_properties_gpu():
     """Symmetry, recurrence and Eq. (deriv) hold on the GPU outputs directly."""
     rng = np.random.default_rng(2)
