@@ -317,11 +317,14 @@ blk_status cuda_fail(cudaError_t e, const char *where) {
 }
 
 int auto_lanes(size_t n, int nbins) {
-  // One element per thread fills the chip once n >= ~148 SMs x 512 threads;
-  // below that, split the bins of each element over a few lanes.
-  const size_t fill = (size_t)148 * 512;
+  // Small batches are latency-bound: splitting each element's nodes over a
+  // few lanes shortens the quadrature (the range finding is repeated per
+  // lane).  Measured on B200 (profiles/r01_lanes_small_batches.log, c2, 128
+  // bins): it pays while n x lanes stays below ~40k threads, up to 8 lanes
+  // (n = 1e3: 8 lanes 10 us vs 14; 1e4: 4 lanes; 2e4: 2; >= 3e4: 1).
+  const size_t fill = 40000;
   int lanes = 1;
-  while (lanes < 32 && n * lanes < fill && (nbins + 1) / (lanes * 2) >= 8) lanes *= 2;
+  while (lanes < 8 && n * lanes * 2 <= fill && (nbins + 1) / (lanes * 2) >= 8) lanes *= 2;
   return lanes;
 }
 
