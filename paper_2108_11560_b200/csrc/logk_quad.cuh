@@ -46,6 +46,10 @@ constexpr int kGroup = BLK_GROUP; // nodes evaluated together (independent exp c
 #define BLK_GROUP2 4
 #endif
 constexpr int kGroup2 = BLK_GROUP2; // v2 loop group size
+#ifndef BLK_V2_UNROLL
+#define BLK_V2_UNROLL 1
+#endif
+constexpr int kV2Unroll = BLK_V2_UNROLL; // tuning knob: unroll of the v2 group loop
 
 // 2^(j/2048) with (j << 9) subtracted from the high word (gen_exp2_table.py):
 // adding (k << 9) to the high word of entry k & 2047 gives 2^(k/2048) for
@@ -326,7 +330,7 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
   }
   double md = (double)ib;
   int m = ib;
-#pragma unroll 1
+#pragma unroll (kV2Unroll)
   for (; m + G <= ie; m += G) {
     const double tc = fma(md, h, t0);
     md += (double)G;
