@@ -547,6 +547,10 @@ blk_status run_host(const T *v, const T *x, size_t n, T *logk, T *dlogk_dv, T *d
   cudaEvent_t start_ev;
   if ((e = cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming)) != cudaSuccess)
     return cuda_fail(e, "cudaEventCreate");
+  struct EventGuard {          // destroyed on every return path
+    cudaEvent_t ev;
+    ~EventGuard() { cudaEventDestroy(ev); }
+  } guard{start_ev};
   cudaEventRecord(start_ev, stream);
   for (int k = 0; k < kHostStreams; ++k) cudaStreamWaitEvent(pool->s[k], start_ev, 0);
   size_t nchunks = (n + chunk - 1) / chunk;
@@ -579,7 +583,6 @@ blk_status run_host(const T *v, const T *x, size_t n, T *logk, T *dlogk_dv, T *d
     cudaEventRecord(pool->ev[k], pool->s[k]);
     cudaStreamWaitEvent(stream, pool->ev[k], 0);
   }
-  cudaEventDestroy(start_ev);
   if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_fail(e, "synchronize");
   return BLK_OK;
 }
