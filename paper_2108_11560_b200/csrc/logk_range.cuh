@@ -287,6 +287,79 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   return p;
 }
 
+// Alg. 2 for the range ends with the search direction a runtime flag (ASC:
+// the t0 search from a = 0 up to t_p; otherwise the t1 search down from the
+// FindRange end), so that two lanes can run the t0 and the t1 search of the
+// same element in one loop (make_plan_f32_pair).  Same updates and stopping
+// rule as find_zero_f32<false, ASC>.
+template <class PF>
+__device__ __forceinline__ float find_zero_f32_rt(const PF &P, float c, float a, float &Fa,
+                                                  float dFa, float b, float tol, float ref,
+                                                  bool asc, bool active) {
+#pragma unroll 1
+  for (int i = 0; active && i < kMaxIter; ++i) {
+    const float rhs = tol * fabsf((a - ref) * dFa);
+    if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
+    const float mid = fmaf(b - a, 0.5f, a);
+    const float t = fmaf(-Fa, rcp_approx(dFa), a);
+    const float tn = asc ? fmaxf(fminf(t, mid), a) : fminf(fmaxf(t, mid), a);
+    float2 F, dF;
+    P.thr2(c, f2(mid, tn), F, dF);
+    fz_update<float>(mid, tn, F.x, dF.x, F.y, dF.y, a, Fa, dFa, b);
+  }
+  return a;
+}
+
+// make_plan_f32 for a PAIR of lanes working on the same element (lanes per
+// element >= 2): both find t_p and g(t_p); then the even lane runs the t0
+// search while the odd lane runs FindRange + the t1 search
+// in the same loop, and the two exchange their ends with a
+// shuffle.  Same ranges as make_plan_f32 (the same arithmetic per search);
+// the latency of one of the two searches is saved, which is what bounds
+// small batches.  All lanes of the pair must be active.
+template <bool NEWTON = false>
+__device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, double log_eps,
+                                                         float tol, bool odd) {
+  Plan<float> p;
+  PlanF32T<NEWTON> P;
+  P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
+  P.m2vs = -2.0f * P.v * PlanF32T<NEWTON>::kL2e; P.L = float(log_eps);
+  float lo, hi, Fh, dFh;
+  p.ok = false;
+  p.tp = 0.0f;
+  if (vd * vd - xd > 0.0) {
+    auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
+    if (!find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
+    p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo, tol);
+  }
+  p.gp = P.gval(p.tp);
+  const float c = p.gp + P.L + float(kLn2);
+  const float d0 = -P.x - p.gp - P.L;                             // d(0)
+  bool range_ok = true;
+  float a, Fa, dFa, b;
+  bool active;
+  if (odd) {                                                      // t1: FindRange first
+    auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
+    range_ok = find_range(df, p.tp, lo, hi, Fh, dFh);
+    a = hi; Fa = Fh; dFa = dFh; b = lo; active = range_ok;
+  } else {                                                        // t0 from 0 (if needed)
+    a = 0.0f; Fa = d0; dFa = 0.0f; b = p.tp; active = d0 <= 0.0f;
+  }
+  a = find_zero_f32_rt(P, c, a, Fa, dFa, b, tol, p.tp, !odd, active);
+  const unsigned mask = __activemask();
+  const float a_o = __shfl_xor_sync(mask, a, 1);
+  const float Fa_o = __shfl_xor_sync(mask, Fa, 1);
+  const bool ok_o = __shfl_xor_sync(mask, (int)range_ok, 1) != 0;
+  const float t0 = odd ? a_o : a, t1 = odd ? a : a_o;
+  const float F0 = odd ? Fa_o : Fa, F1 = odd ? Fa : Fa_o;
+  if (!(odd ? range_ok : ok_o)) return p;
+  p.t0 = (d0 <= 0.0f) ? t0 : 0.0f;
+  p.t1 = t1;
+  p.dmin = fminf(d0 <= 0.0f ? F0 : d0, F1);
+  p.ok = true;
+  return p;
+}
+
 // ==================================================================== FP64
 struct PlanF64 {
   double v, x, hx, v2, m2v;
