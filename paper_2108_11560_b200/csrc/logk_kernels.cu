@@ -158,7 +158,8 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
+      const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
+                                       : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
@@ -209,7 +210,9 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   bool ok = false;
   if (valid) {
     if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
-      const Plan<float> p = make_plan_f32<BLK_F32_NEWTON>(v, x, kLogEpsF32, fz_tol_for(nbins));
+      const Plan<float> p =
+          (LPE >= 2) ? make_plan_f32_pair<BLK_F32_NEWTON>(v, x, kLogEpsF32, fz_tol_for(nbins), sub & 1)
+                     : make_plan_f32<BLK_F32_NEWTON>(v, x, kLogEpsF32, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);
