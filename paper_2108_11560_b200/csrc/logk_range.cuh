@@ -346,7 +346,10 @@ __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, 
     a = 0.0f; Fa = d0; dFa = 0.0f; b = p.tp; active = d0 <= 0.0f;
   }
   a = find_zero_f32_rt(P, c, a, Fa, dFa, b, tol, p.tp, !odd, active);
-  const unsigned mask = __activemask();
+  // the two lanes of the pair, named explicitly: they may leave the search
+  // loop at different iterations, and __shfl_xor_sync with this mask waits
+  // for both (an __activemask() taken here could miss the partner)
+  const unsigned mask = 3u << ((threadIdx.x & 31u) & ~1u);
   const float a_o = __shfl_xor_sync(mask, a, 1);
   const float Fa_o = __shfl_xor_sync(mask, Fa, 1);
   const bool ok_o = __shfl_xor_sync(mask, (int)range_ok, 1) != 0;
