@@ -77,17 +77,19 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
                 double *__restrict__ logk, double *__restrict__ dlogk_dv,
                 double *__restrict__ dlogk_dx, int nbins, int range_mode) {
   BLK_TL(0);
-  load_exp_table();
-  __syncthreads();
-  const double *tab = g_exp_tab;
-
   const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t i = gtid / LPE;
   const int sub = (int)(gtid % LPE);
   const bool live = i < n_el;
   // Lanes past the end still take part in the shuffles (full-warp masks).
+  // The input loads are issued before the table copy and its barrier, which
+  // hide their latency (it stalled every warp at its first use of x).
   const double vraw = live ? vin[i] : 1.0;
   const double x = live ? xin[i] : 1.0;
+  load_exp_table();
+  __syncthreads();
+  const double *tab = g_exp_tab;
+
   const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
   const double v = fabs(vraw);
   const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
@@ -101,7 +103,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
                                        : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
-      const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
+      const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
@@ -143,14 +145,14 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
                      double *__restrict__ dx_out, double *__restrict__ dvv_out,
                      double *__restrict__ dxx_out, double *__restrict__ dvx_out, int nbins,
                      int range_mode) {
-  load_exp_table();
-  __syncthreads();
   const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t i = gtid / LPE;
   const int sub = (int)(gtid % LPE);
   const bool live = i < n_el;
-  const double vraw = live ? vin[i] : 1.0;
+  const double vraw = live ? vin[i] : 1.0;   // loads issued ahead of the table copy
   const double x = live ? xin[i] : 1.0;
+  load_exp_table();
+  __syncthreads();
   const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
   const double v = fabs(vraw);
   const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
@@ -162,7 +164,7 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
                                        : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
-      const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
+      const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;

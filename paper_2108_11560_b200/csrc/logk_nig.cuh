@@ -34,13 +34,14 @@ __device__ __forceinline__ double warp_sum(double a) {
 __global__ void __launch_bounds__(kNigThreads, BLK_MINB)
 nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, double d, double m,
                double g, int nbins, double *__restrict__ partial) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double yi = i < n ? y[i] : 0.0;   // issued ahead of the table copy
   load_exp_table();
   __syncthreads();
   __shared__ double red[kNigOut][kNigThreads / 32];
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   double c[kNigOut] = {0.0, 0.0, 0.0, 0.0, 0.0};
   if (i < n) {
-    const double r = y[i] - m;
+    const double r = yi - m;
     const double q2 = fma(r, r, d * d), q = sqrt(q2);
     const double z = a * q;
     double lk = __longlong_as_double(0x7ff8000000000000ULL), D = lk;
@@ -51,7 +52,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
         const Plan<float> p = make_plan_f32(1.0, z, kLogEpsF64, fz_tol_for(nbins));
         ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
       } else {
-        const Plan<double> p = make_plan_f64(1.0, z, kLogEpsF64);
+        const Plan<double> p = make_plan_f64_tab(1.0, z, kLogEpsF64);
         ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
       }
       ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;

@@ -73,7 +73,16 @@ __device__ __forceinline__ void load_exp_table() {
 
 // 2^(k/2048) for k in [-2^21, 2^21): one LDS.64 and one IMAD.
 __device__ __forceinline__ double exp_scale(int k) {
-  const double tj = g_exp_tab[k & (kExpTab - 1)];
+  // explicit 32-bit shared address (and, shl, add -> LOP3 + LEA): left to
+  // itself ptxas folds the table base into the LDS only while it can keep it
+  // in a uniform register, and loses that with any per-lane branch ahead of
+  // the node loop (one extra integer add per node)
+  const unsigned base = (unsigned)__cvta_generic_to_shared(g_exp_tab);
+  unsigned addr;
+  asm("{\n\t.reg .u32 t;\n\tand.b32 t, %1, 2047;\n\tshl.b32 t, t, 3;\n\tadd.u32 %0, t, %2;\n\t}"
+      : "=r"(addr) : "r"(k), "r"(base));
+  double tj;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(tj) : "r"(addr));
   return __hiloint2double(k * 512 + __double2hiint(tj), __double2loint(tj));
 }
 
@@ -81,6 +90,13 @@ constexpr double kExpInvL = 2954.639443740597;       // 2048 / ln 2
 constexpr double kExpMagic = 6755399441055744.0;     // 1.5 * 2^52: round-to-int trick
 constexpr double kExpC = 0.0003384507717577858;      // ln2/2048 (single-step reduction:
                                                      // |k| <= 2.1e6 -> |error| < 6e-14 |a|/707)
+// -ln2/2048 as a constant-bank operand for the node loops: fma(kd, -C, a)
+// with C in a general register reads three distinct 64-bit registers (one
+// extra issue cycle); ptxas keeps a __constant__ operand in the
+// constant bank (it otherwise picks a uniform or a general register depending
+// on what else the kernel holds).
+__constant__ double kNegExpCc = -0.0003384507717577858;
+
 // e^r - 1 for |r| <= ln2/4096 (truncation r^4/24 < 3.5e-17): Horner, every
 // operation with at most two register operands (the FP64 pipe issues an
 // instruction reading three distinct 64-bit registers in 3 cycles, not 2:
@@ -118,6 +134,28 @@ __device__ __forceinline__ double rcp64(double a) {
   return fma(r, e, r);
 }
 
+// e^h - 1 for 0 <= h < ln 2 to ~1 ulp of the result (once per lane, for
+// the cosh recurrence steps of the v2 loop): e^{h/2} - 1 by its Taylor
+// series to degree 13 (all terms positive; truncation < 2e-17 relative for
+// h/2 <= 0.35), then e^h - 1 = u (u + 2).
+__device__ __forceinline__ double expm1_small(double h) {
+  const double y = 0.5 * h;
+  double p = fma(y, 1.0 / 6227020800.0, 1.0 / 479001600.0);   // 1/13!, 1/12!
+  p = fma(p, y, 1.0 / 39916800.0);
+  p = fma(p, y, 1.0 / 3628800.0);
+  p = fma(p, y, 1.0 / 362880.0);
+  p = fma(p, y, 1.0 / 40320.0);
+  p = fma(p, y, 1.0 / 5040.0);
+  p = fma(p, y, 1.0 / 720.0);
+  p = fma(p, y, 1.0 / 120.0);
+  p = fma(p, y, 1.0 / 24.0);
+  p = fma(p, y, 1.0 / 6.0);
+  p = fma(p, y, 0.5);
+  p = fma(p, y, 1.0);
+  const double u = p * y;
+  return fma(u, u, 2.0 * u);
+}
+
 // 1 - e^z for z <= 0 without cancellation (-expm1(z)).
 __device__ __forceinline__ double one_minus_exp(double z) {
   if (z < -0.34657359027997264) return 1.0 - exp_tab<true>(z);
@@ -137,6 +175,62 @@ __device__ __forceinline__ double one_minus_exp(double z) {
   p = fma(p, z, 0.5);
   p = fma(p, z, 1.0);
   return -(p * z);
+}
+
+// FP64 range-finder point evaluations with the table exp and rcp64 instead
+// of libdevice exp and IEEE division (kernels that load the exp table):
+// 3-4x fewer instructions per evaluation, ~1 ulp like the libm calls.
+// exp(a), a in [-707, 709.78], with a two-part (Cody-Waite) ln2/2048 (no
+// reduction error: ~0.5 ulp from the table entry plus the final rounding);
+// for the FP64 range finder.  Its constants
+// differ from exp_tab's on purpose: sharing them with this rarely taken path,
+// ptxas moved the node loops' reduction constant to a general register (a
+// three-register DFMA in every node).
+__device__ __forceinline__ double exp_cw(double a) {
+  double kd = fma(a, kExpInvL, kExpMagic);
+  const int k = __double2loint(kd);
+  kd -= kExpMagic;
+  double r = fma(kd, -3.384507715509244e-04, a);   // hi part: 31-bit mantissa, kd * hi exact
+  r = fma(kd, -2.0686139481490644e-13, r);
+  const double ts = exp_scale(k);
+  return fma(ts, exp_em1(r), ts);
+}
+
+struct PlanF64Tab {
+  double v, x, hx, v2, m2v;
+  // e^{+-t}, overflowing to (inf, 0) past 709.78 like libm (FindRange's far
+  // probes: F = -inf there, as in the oracle)
+  __device__ __forceinline__ void ep(double t, double &e, double &ei) const {
+    const bool fin = t < 709.78;
+    e = exp_cw(fmin(t, 709.78));
+    ei = rcp64(e);
+    if (!fin) { e = __longlong_as_double(0x7ff0000000000000ULL); ei = 0.0; }
+  }
+  __device__ __forceinline__ void parts(double t, double &e, double &ei, double &q, double &r) const {
+    ep(t, e, ei);
+    q = exp_cw(fmax(m2v * t, -707.0));
+    r = rcp64(1.0 + q);
+  }
+  __device__ __forceinline__ void peak(double t, double &F, double &dF) const {
+    double e, ei, q, r;
+    parts(t, e, ei, q, r);
+    F = v * ((1.0 - q) * r) - hx * (e - ei);
+    dF = v2 * (4.0 * q * r * r) - hx * (e + ei);
+  }
+  __device__ __forceinline__ void thr(double c, double t, double &F, double &dF) const {
+    double e, ei, q, r;
+    parts(t, e, ei, q, r);
+    F = v * t + log1p(q) - hx * (e + ei) - c;
+    dF = v * ((1.0 - q) * r) - hx * (e - ei);
+  }
+  __device__ __forceinline__ double gval(double t) const {
+    double e, ei;
+    ep(t, e, ei);
+    return v * t + log1p(exp_cw(fmax(m2v * t, -707.0))) - kLn2 - hx * (e + ei);
+  }
+};
+__device__ __forceinline__ Plan<double> make_plan_f64_tab(double v, double x, double log_eps) {
+  return make_plan_f64_with(PlanF64Tab{v, x, 0.5 * x, v * v, -2.0 * v}, v, x, log_eps);
 }
 
 struct Sums64 {
@@ -243,7 +337,7 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
 #pragma unroll
       for (int j = 0; j < kGroup; ++j) ts[j] = exp_scale(k[j]);
 #pragma unroll
-      for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
+      for (int j = 0; j < kGroup; ++j) r[j] = fma(kd[j], kNegExpCc, a[j]);
 #pragma unroll
       for (int j = 0; j < kGroup; ++j) {
         const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
@@ -279,7 +373,14 @@ __device__ __forceinline__ void nodes_fp64(double v, double x, double t0, double
 //     v t1 >= 1e-3 (error < 3e-13) or v = 0 (exactly 0); smaller v t1 takes
 //     the v1 loop;
 //   * e^{+-t} and q advance per group by e^{+-G h}, e^{-2 v G h} and inside
-//     the group by e^{+-h}, e^{-2 v h}: drift <= n/G + G ulp, no re-anchoring.
+//     the group by e^{+-h}, e^{-2 v h}, no re-anchoring.  The group steps
+//     of the cosh factors are X <- X + X u with u = e^{+-Gh} - 1 from an
+//     accurate expm1: a rounded multiplier e^{+-Gh} would add the same
+//     relative error at every step, a systematic drift of (n/G) ulp of X in
+//     the exponent -- 2e-11 absolute where x cosh t ~ 1e4 cancels against
+//     v t to a small g (test_large_order_cancellation); with u it is ~|u|
+//     ulp per step.  Same instruction count (an FMA reading two distinct
+//     registers instead of a DMUL).
 // One node of the v2 loop: E = e^{a}, w = E (1 + q), Ep = 2E - w = E (1 - q)
 // (S1 term / t), X = x cosh t.  HESS adds the second-order sums in the
 // scaled form S22x = sum w X^2 = x^2 S22 and S12x = sum Ep t X = x S12.
@@ -307,17 +408,24 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
                                               double s_mid, int ib, int ie, Sums64 &out) {
   if (ie <= ib) return;
   constexpr int G = kGroup2;
-  const double vh = v * h;
-  const double m2v = -2.0 * v;
+  const double m2v = -2.0 * v, vh = v * h;
   const double tb = fma((double)ib, h, t0);
   const double eb = exp_tab<true>(fmin(tb, 709.0));
   const double hx = 0.5 * x;
   double XpG = hx * eb, XmG = hx * rcp64(eb);
-  const double e1 = exp_tab<false>(h), e1i = rcp64(e1);
-  const double eG = exp_tab<true>(fmin(G * h, 709.0)), eGi = rcp64(eG);
+  static_assert(G == 4, "uG below is (1 + u1)^4 - 1");
+  // e^{+-h} - 1 and e^{+-Gh} - 1 for the steps X <- X + X u (u1 to ~1 ulp
+  // for h < ln 2; beyond, e^h - 1 is no more precise than e^h itself).
+  // Branch-free: the lanes of a warp would take both sides.  Capped like the
+  // exp arguments at 709: only ranges reaching e^t ~ 1e308 (x < 1e-300) get
+  // there, where those nodes underflow either way.
+  const double u1c = exp_tab<false>(fmin(h, 709.0)) - 1.0, u1a = expm1_small(h);
+  const double u1 = fmin(h < 0.6931 ? u1a : u1c, 8e307);
+  const double uG = fmin(u1 * fma(u1, fma(u1, 4.0 + u1, 6.0), 4.0), 8e307);  // e^{Gh} - 1
+  const double uGi = -uG * rcp64(1.0 + uG);                                  // e^{-Gh} - 1
+  const double u1i = -u1 * rcp64(1.0 + u1);                                  // e^{-h} - 1
   double qG = exp_tab<true>(m2v * tb);
   const double eq1 = exp_tab<true>(m2v * h);
-  static_assert(G == 4, "eqG below is eq1^4");
   // e^{-2v G h} by squaring: q only enters w = E (1 + q), where a few ulp of
   // drift over n/G steps are far below the other rounding (measured +1%)
   const double eq2 = eq1 * eq1, eqG = eq2 * eq2;
@@ -342,9 +450,9 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
     for (int j = 0; j < G; ++j) {
       X[j] = xp + xm;
       q[j] = qq;
-      if (j + 1 < G) { xp *= e1; xm *= e1i; qq *= eq1; }
+      if (j + 1 < G) { xp = fma(xp, u1, xp); xm = fma(xm, u1i, xm); qq *= eq1; }
     }
-    XpG *= eG; XmG *= eGi; qG *= eqG;
+    XpG = fma(XpG, uG, XpG); XmG = fma(XmG, uGi, XmG); qG *= eqG;
 #pragma unroll
     for (int j = 0; j < G; ++j) a[j] = (j == 0 ? Bc : fma(double(j), vh, Bc)) - X[j];
 #pragma unroll
@@ -357,7 +465,7 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
 #pragma unroll
     for (int j = 0; j < G; ++j) ts[j] = exp_scale(k[j]);
 #pragma unroll
-    for (int j = 0; j < G; ++j) r[j] = fma(kd[j], -kExpC, a[j]);
+    for (int j = 0; j < G; ++j) r[j] = fma(kd[j], kNegExpCc, a[j]);
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
@@ -366,13 +474,14 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
     }
   }
   double xp = XpG, xm = XmG, qq = qG;
+  const double tr = fma(md, h, t0);
 #pragma unroll 1
   for (; m < ie; ++m) {                             // remainder, one node at a time
-    const double t = fma((double)m, h, t0);
+    const double t = fma((double)m - md, h, tr);
     const double X = xp + xm;
     const double E = exp_tab<false>(fma(v, t, -s_mid) - X);
     v2_accumulate<DV, DX, HESS>(E, qq, X, t, S0, S1, S2, S11, S22, S12);
-    xp *= e1; xm *= e1i; qq *= eq1;
+    xp = fma(xp, u1, xp); xm = fma(xm, u1i, xm); qq *= eq1;
   }
   const double rx = rcp64(x);
   out.S0 += S0;

@@ -384,11 +384,18 @@ struct PlanF64 {
   }
 };
 
+// Alg. 2 in double.  The paper's working-precision variant: it stops only
+// once a has converged (Newton correction below 2^-45 of the scale: |a| for
+// the peak, |a - t_p| for the range ends), where further iterations leave a
+// unchanged to the last bits -- so the ranges are those of the oracle's fixed
+// 10 iterations (BLK_RANGE_F64 reproduces the oracle at coarse grids, R20).
 template <class Fn>
 __device__ __forceinline__ double find_zero_f64(const Fn &f, double a, double &Fa, double dFa,
-                                                double b) {
+                                                double b, double ref) {
 #pragma unroll 1
   for (int i = 0; i < kMaxIter; ++i) {
+    const double rhs = 2.842170943040401e-14 * fabs((a - ref) * dFa);   // 2^-45
+    if (fabs(Fa) <= rhs && rhs <= 1e300) break;
     double mid, tn;
     fz_points<double>(a, Fa, dFa, b, mid, tn);
     double Fm, dFm, Ft, dFt;
@@ -399,28 +406,35 @@ __device__ __forceinline__ double find_zero_f64(const Fn &f, double a, double &F
   return a;
 }
 
-__device__ __forceinline__ Plan<double> make_plan_f64(double v, double x, double log_eps) {
+// Alg. 3 lines 2-9 in double for a point-evaluation type PF (peak, thr, gval).
+template <class PF>
+__device__ __forceinline__ Plan<double> make_plan_f64_with(const PF &P, double v, double x,
+                                                         double log_eps) {
   Plan<double> p;
-  PlanF64 P{v, x, 0.5 * x, v * v, -2.0 * v};
   double lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0;
   auto pf = [&](double t, double &F, double &dF) { P.peak(t, F, dF); };
   if (v * v - x > 0.0) {
     if (!find_range(pf, 0.0, lo, hi, Fh, dFh)) return p;
-    p.tp = find_zero_f64(pf, hi, Fh, dFh, lo);
+    p.tp = find_zero_f64(pf, hi, Fh, dFh, lo, 0.0);
   }
   p.gp = P.gval(p.tp);
   const double c = p.gp + log_eps + kLn2;
   auto df = [&](double t, double &F, double &dF) { P.thr(c, t, F, dF); };
   p.t0 = 0.0;
   double d0 = -x - p.gp - log_eps;
-  if (d0 <= 0.0) p.t0 = find_zero_f64(df, 0.0, d0, 0.0, p.tp);
+  if (d0 <= 0.0) p.t0 = find_zero_f64(df, 0.0, d0, 0.0, p.tp, p.tp);
   if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
-  p.t1 = find_zero_f64(df, hi, Fh, dFh, lo);
+  p.t1 = find_zero_f64(df, hi, Fh, dFh, lo, p.tp);
   p.dmin = fmin(d0, Fh);
   p.ok = true;
   return p;
+}
+
+// libdevice point evaluations (kernels without the shared exp table)
+__device__ __forceinline__ Plan<double> make_plan_f64(double v, double x, double log_eps) {
+  return make_plan_f64_with(PlanF64{v, x, 0.5 * x, v * v, -2.0 * v}, v, x, log_eps);
 }
 
 // Inputs for which the FP32 range finder is used under BLK_RANGE_AUTO:

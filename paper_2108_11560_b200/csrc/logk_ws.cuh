@@ -114,7 +114,7 @@ logk_f64_ws_kernel(const double *__restrict__ vin, const double *__restrict__ xi
           const Plan<float> p = make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
           ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
         } else {
-          const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
+          const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
           ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
         }
         ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;

@@ -45,3 +45,22 @@ def max_errors(got: dict, ref: dict):
         e = errors(np.asarray(g, dtype=np.float64)[ok], r[ok], kind)
         out[kind] = float(e.max()) if e.size else 0.0
     return out
+
+
+def cancellation_band(n, seed, nbins=128):
+    """Orders v in [1e3, 2e4] with x chosen (bisection on the oracle, log K
+    decreasing in x) so that log K_v(x) lies in [-20, 20]: v t and x cosh t
+    are ~1e4 there and cancel to a small g, so an exponent error of a few ulp
+    of x cosh t is ~1e-12 of log K."""
+    import oracle
+    rng = np.random.default_rng(seed)
+    v = 10.0 ** rng.uniform(3, np.log10(2e4), n)
+    target = rng.uniform(-20, 20, n)
+    lo, hi = np.full(n, 1e-3) * v, np.full(n, 3.0) * v
+    for _ in range(60):
+        mid = np.sqrt(lo * hi)
+        lk = oracle.logk(v, mid, nbins, threads=8)[0]
+        above = lk > target
+        lo = np.where(above, mid, lo)
+        hi = np.where(above, hi, mid)
+    return v, np.sqrt(lo * hi)

@@ -386,8 +386,9 @@ def test_wide_domain_fuzz(seed):
     tol_d = np.maximum(1e-10, 10 * kappa)
     assert np.array_equal(np.isnan(got["logk"]), np.isnan(lk))
     ok = ~np.isnan(lk)
+    tol_l = np.maximum(1e-12, kappa[ok] / np.maximum(1.0, np.abs(lk[ok])))
     e0 = errors(got["logk"][ok], lk[ok], "logk")
-    assert e0.max() <= 1e-12, (e0.max(), v[ok][np.argmax(e0)], x[ok][np.argmax(e0)])
+    assert np.all(e0 <= tol_l), (e0.max(), v[ok][np.argmax(e0)], x[ok][np.argmax(e0)])
     e2 = errors(got["dx"][ok], dx[ok], "dx")
     assert np.all(e2 <= tol_d[ok]), (v[ok][np.argmax(e2 / tol_d[ok])], x[ok][np.argmax(e2 / tol_d[ok])])
     e1 = errors(got["dv"][ok], dv[ok], "dv")
@@ -559,3 +560,36 @@ def test_cuda_graph_capture():
     torch.cuda.synchronize()
     for a, b in zip(outs, ref):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 0])
+def test_large_order_cancellation(lanes):
+    """log K where x cosh t ~ 1e4 cancels against v t (found by the wide-domain
+    fuzz at v = 18140, x = 12025): the v2 loop steps the cosh factors with
+    accurate e^{+-h} - 1 (fma(X, u, X)) instead of a rounded e^{+-h}, whose
+    rounding drifted the exponent by (n/G) ulp of x cosh t -- 2.2e-11 at one
+    lane per element, 7x the floor eps (x + v t_p); the build before that
+    change fails this test at lanes 1 and 2."""
+    from parity import cancellation_band
+    v, x = cancellation_band(256, 7)
+    got = run_gpu(v, x, lanes_per_element=lanes)
+    lk, dv, dx, plan = oracle.logk(v, x, NB, with_plan=True, threads=8)
+    from parity import errors
+    assert np.all(np.abs(lk) <= 25.0)
+    # kappa = eps (x + v t_p), one rounding of the exponent's ~1e4 terms, is
+    # the floor of any double evaluation (DESIGN.md §3 tolerance note).  The
+    # oracle's independent per-node roundings average to <= 0.45 kappa
+    # (test_oracle_pins); the kernel's B_c = v t_c - s and start state are
+    # shared by a group / a lane, and a peak this narrow spans ~2 groups, so
+    # they average less: log K is held to 2 kappa against the long-double
+    # brute force and 2.5 kappa against the oracle.
+    kappa = np.finfo(float).eps * (x + v * plan[:, 0] + 40.0)
+    tol_l = np.maximum(1e-12, kappa / np.maximum(1.0, np.abs(lk)))
+    lk_b = oracle.brute(v, x, threads=8)[0]
+    eb = errors(got["logk"], lk_b, "logk")
+    assert np.all(eb <= 2 * tol_l), ((eb / tol_l).max(), v[np.argmax(eb / tol_l)], x[np.argmax(eb / tol_l)])
+    e0 = errors(got["logk"], lk, "logk")
+    assert np.all(e0 <= 2.5 * tol_l), ((e0 / tol_l).max(), v[np.argmax(e0 / tol_l)])
+    tol_d = np.maximum(1e-10, 10 * kappa)
+    assert np.all(errors(got["dv"], dv, "dv") <= tol_d)
+    assert np.all(errors(got["dx"], dx, "dx") <= tol_d)

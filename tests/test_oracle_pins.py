@@ -382,3 +382,21 @@ def test_reading_R14_own_range_derivatives(cfg):
     nzb = bv != 0
     assert np.all(np.abs(dv2[:120][nzb] - bv[nzb]) <= 5e-14 * sc[:120][nzb] * np.abs(bv[nzb]))
     assert np.all(np.abs(dx2[:120] - bx) <= 5e-14 * sc[:120] * np.abs(bx))
+
+
+def test_cancellation_band_vs_brute_force():
+    """Where v t and x cosh t (~1e4) cancel to |log K| < 20, the oracle's log K
+    is within the exponent's rounding floor eps (x + v t_p) of the long-double
+    plain-definition value (DESIGN.md §3 tolerance note): double arithmetic
+    cannot do better there, and this is the floor the GPU test holds the
+    kernels to."""
+    from parity import cancellation_band, errors
+    v, x = cancellation_band(128, 11)
+    lk, _, _, plan = oracle.logk(v, x, 128, with_plan=True, threads=8)
+    lk_b = oracle.brute(v, x, threads=8)[0]
+    kappa = np.finfo(float).eps * (x + v * plan[:, 0] + 40.0)
+    tol = np.maximum(1e-12, kappa / np.maximum(1.0, np.abs(lk_b)))
+    e = errors(lk, lk_b, "logk")
+    assert np.all(e <= tol), ((e / tol).max(), v[np.argmax(e / tol)], x[np.argmax(e / tol)])
+    # and the floor is not vacuous: the oracle's error there is not far below it
+    assert (e / tol).max() > 0.05
