@@ -130,7 +130,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   // a7: epilogue
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
   const double r = rcp64(s.S0);
-  if (LOGK) logk[i] = ok ? gp + log(h * s.S0) : nanv;
+  if (LOGK) logk[i] = ok ? gp + log_sum(h * s.S0) : nanv;
   if (DV) dlogk_dv[i] = ok ? sgn * (s.S1 * r) : nanv;
   if (DX) dlogk_dx[i] = ok ? -(s.S2 * r) : nanv;
 }
@@ -185,7 +185,7 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
   const double r = rcp64(s.S0);
   const double m1 = s.S1 * r, m2 = s.S2 * r;
-  if (logk) logk[i] = ok ? gp + log(h * s.S0) : nanv;
+  if (logk) logk[i] = ok ? gp + log_sum(h * s.S0) : nanv;
   if (dv_out) dv_out[i] = ok ? sgn * m1 : nanv;
   if (dx_out) dx_out[i] = ok ? -m2 : nanv;
   if (dvv_out) dvv_out[i] = ok ? fma(-m1, m1, s.S11 * r) : nanv;

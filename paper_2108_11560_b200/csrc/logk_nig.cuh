@@ -62,7 +62,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
                              ? quad_f64<false, true, false>(1.0, z, t0, h, gp, nbins, 0, nbins + 1, g_exp_tab)
                              : quad_f64<false, true, true>(1.0, z, t0, h, gp, nbins, 0, nbins + 1, g_exp_tab);
         const double rs = rcp64(s.S0);
-        lk = gp + log(h * s.S0);
+        lk = gp + log_sum(h * s.S0);
         D = -(s.S2 * rs);
       }
     }

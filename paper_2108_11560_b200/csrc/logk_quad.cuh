@@ -90,6 +90,7 @@ constexpr double kExpInvL = 2954.639443740597;       // 2048 / ln 2
 constexpr double kExpMagic = 6755399441055744.0;     // 1.5 * 2^52: round-to-int trick
 constexpr double kExpC = 0.0003384507717577858;      // ln2/2048 (single-step reduction:
                                                      // |k| <= 2.1e6 -> |error| < 6e-14 |a|/707)
+constexpr double kExpClo = 1.1323470770733885e-20;   // ln2/2048 - kExpC
 // -ln2/2048 as a constant-bank operand for the node loops: fma(kd, -C, a)
 // with C in a general register reads three distinct 64-bit registers (one
 // extra issue cycle); ptxas keeps a __constant__ operand in the
@@ -154,6 +155,34 @@ __device__ __forceinline__ double expm1_small(double h) {
   p = fma(p, y, 1.0);
   const double u = p * y;
   return fma(u, u, 2.0 * u);
+}
+
+// log(y) for normal positive y with the exp table (the epilogue's
+// log(h S0)): y = 2^e m, m in [1, 2); k = round(2048 log2 m) from MUFU.LG2,
+// m 2^{-k/2048} = 1 + r with |r| < 2^-11 (the table entry for -k), log1p(r)
+// by its series to r^5 (truncation < 1e-19 relative), and (2048 e + k) ln2/2048
+// with a two-part constant.  ~2 ulp of the table entry and the product: an
+// absolute error < 3e-16, against ~29 FP64 instructions for libdevice log.
+__device__ __forceinline__ double log_tab(double y) {
+  const int hi = __double2hiint(y);
+  const int e = (hi >> 20) - 1023;
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(y));
+  float l2;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(__double2float_rn(m)));
+  const int k = __float2int_rn(l2 * 2048.0f);            // 0 .. 2048
+  const double r = m * exp_scale(-k) - 1.0;
+  double p = fma(r, 0.2, -0.25);
+  p = fma(p, r, 1.0 / 3.0);
+  p = fma(p, r, -0.5);
+  const double l1 = fma(p * r, r, r);
+  const double kk = (double)(e * 2048 + k);
+  return fma(kk, kExpC, fma(kk, kExpClo, l1));
+}
+
+// log(y) of the epilogue's y = h S0: log_tab on normal finite y, libm for the
+// rest (0, subnormal, inf: not reached by valid ranges).
+__device__ __forceinline__ double log_sum(double y) {
+  return (y >= 2.2250738585072014e-308 && y < 1.7e308) ? log_tab(y) : log(y);
 }
 
 // 1 - e^z for z <= 0 without cancellation (-expm1(z)).
@@ -422,8 +451,8 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
   const double u1c = exp_tab<false>(fmin(h, 709.0)) - 1.0, u1a = expm1_small(h);
   const double u1 = fmin(h < 0.6931 ? u1a : u1c, 8e307);
   const double uG = fmin(u1 * fma(u1, fma(u1, 4.0 + u1, 6.0), 4.0), 8e307);  // e^{Gh} - 1
-  const double uGi = -uG * rcp64(1.0 + uG);                                  // e^{-Gh} - 1
   const double u1i = -u1 * rcp64(1.0 + u1);                                  // e^{-h} - 1
+  const double uGi = u1i * fma(u1i, fma(u1i, 4.0 + u1i, 6.0), 4.0);          // e^{-Gh} - 1
   double qG = exp_tab<true>(m2v * tb);
   const double eq1 = exp_tab<true>(m2v * h);
   // e^{-2v G h} by squaring: q only enters w = E (1 + q), where a few ulp of

@@ -64,7 +64,7 @@ quad_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
   const double rc = rcp64(r.S0);
   const double sgn = (pl.flags & 4) ? -1.0 : 1.0;
-  if (LOGK) logk[i] = ok ? pl.gp + log(pl.h * r.S0) : nanv;
+  if (LOGK) logk[i] = ok ? pl.gp + log_sum(pl.h * r.S0) : nanv;
   if (DV) dlogk_dv[i] = ok ? sgn * (r.S1 * rc) : nanv;
   if (DX) dlogk_dx[i] = ok ? -(r.S2 * rc) : nanv;
 }

@@ -152,7 +152,7 @@ logk_f64_ws_kernel(const double *__restrict__ vin, const double *__restrict__ xi
         const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
         const double rc = rcp64(r.S0);
         const double sgn = (sl.flags & 4) ? -1.0 : 1.0;
-        if (LOGK) logk[i] = ok ? sl.gp + log(sl.h * r.S0) : nanv;
+        if (LOGK) logk[i] = ok ? sl.gp + log_sum(sl.h * r.S0) : nanv;
         if (DV) dlogk_dv[i] = ok ? sgn * (r.S1 * rc) : nanv;
         if (DX) dlogk_dx[i] = ok ? -(r.S2 * rc) : nanv;
       }
