@@ -81,8 +81,11 @@ __device__ __forceinline__ double exp_scale(int k) {
   unsigned addr;
   asm("{\n\t.reg .u32 t;\n\tand.b32 t, %1, 2047;\n\tshl.b32 t, t, 3;\n\tadd.u32 %0, t, %2;\n\t}"
       : "=r"(addr) : "r"(k), "r"(base));
+  // volatile: the compiler must not move the read above the barrier that
+  // follows load_exp_table (a plain asm is free to move, it has no memory
+  // dependence)
   double tj;
-  asm("ld.shared.f64 %0, [%1];" : "=d"(tj) : "r"(addr));
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(tj) : "r"(addr));
   return __hiloint2double(k * 512 + __double2hiint(tj), __double2loint(tj));
 }
 
@@ -206,15 +209,12 @@ __device__ __forceinline__ double one_minus_exp(double z) {
   return -(p * z);
 }
 
-// FP64 range-finder point evaluations with the table exp and rcp64 instead
-// of libdevice exp and IEEE division (kernels that load the exp table):
-// 3-4x fewer instructions per evaluation, ~1 ulp like the libm calls.
 // exp(a), a in [-707, 709.78], with a two-part (Cody-Waite) ln2/2048 (no
 // reduction error: ~0.5 ulp from the table entry plus the final rounding);
-// for the FP64 range finder.  Its constants
-// differ from exp_tab's on purpose: sharing them with this rarely taken path,
-// ptxas moved the node loops' reduction constant to a general register (a
-// three-register DFMA in every node).
+// for the FP64 range finder.  Its constants differ from exp_tab's on
+// purpose: sharing them with this rarely taken path, ptxas moved the node
+// loops' reduction constant to a general register (a three-register DFMA in
+// every node).
 __device__ __forceinline__ double exp_cw(double a) {
   double kd = fma(a, kExpInvL, kExpMagic);
   const int k = __double2loint(kd);
@@ -225,6 +225,9 @@ __device__ __forceinline__ double exp_cw(double a) {
   return fma(ts, exp_em1(r), ts);
 }
 
+// FP64 range-finder point evaluations with the table exp and rcp64 instead
+// of libdevice exp and IEEE division (kernels that load the exp table):
+// 3-4x fewer instructions per evaluation, ~1 ulp like the libm calls.
 struct PlanF64Tab {
   double v, x, hx, v2, m2v;
   // e^{+-t}, overflowing to (inf, 0) past 709.78 like libm (FindRange's far
