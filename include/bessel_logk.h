@@ -124,16 +124,25 @@ BLK_API blk_status bessel_logk_f32_ex(const float *v, const float *x, size_t n,
 
 /*
  * Host-buffer entry point (end-to-end use).  v, x, logk, dlogk_dv, dlogk_dx
- * are HOST pointers (page-locked memory overlaps copies with compute;
- * pageable memory works but serialises).  The batch is split into chunks of
- * `chunk` elements (0 = default 2^20) that are copied host->device, computed
- * and copied device->host on a small pool of streams so that transfers of one
- * chunk overlap the kernel of another.  workspace: DEVICE buffer of at least
- * bessel_logk_host_workspace_bytes(chunk, 8) bytes, owned by the caller.
+ * are HOST pointers.  Two transports, same results:
+ *  - zero-copy: when every non-NULL buffer is page-locked host memory mapped
+ *    into the device address space (cudaHostAlloc / cudaMallocHost /
+ *    cudaHostRegister under unified addressing -- e.g. torch pin_memory), one
+ *    kernel launch reads the inputs and writes the outputs over PCIe
+ *    directly, so the transfers overlap the computation element by element
+ *    (the workspace is not touched);
+ *  - staged: otherwise (pageable memory works but serialises), the batch is
+ *    split into chunks of `chunk` elements (0 = default 2^20) that are copied
+ *    host->device, computed and copied device->host on a small pool of
+ *    streams so that transfers of one chunk overlap the kernel of another.
+ *    (BLK_HOST_PIPELINE=1 in the environment forces this path; measurement
+ *    only.)
+ * workspace: DEVICE buffer of at least bessel_logk_host_workspace_bytes(chunk,
+ * 8) bytes, owned by the caller (required on both transports).
  * Blocking: returns after all results are in host memory (the work is ordered
- * after prior work on `stream`).  Every chunk runs the simple kernel with one
- * element per lane, so results equal bessel_logk_f64_ex with
- * lanes_per_element = 1 bit for bit, whatever the chunking.
+ * after prior work on `stream`).  Both transports run the simple kernel with
+ * one element per lane, so results equal bessel_logk_f64_ex with
+ * lanes_per_element = 1 bit for bit, whatever the transport or chunking.
  */
 BLK_API size_t bessel_logk_host_workspace_bytes(size_t chunk, size_t elem_bytes);
 BLK_API blk_status bessel_logk_f64_host(const double *v, const double *x, size_t n,

@@ -192,25 +192,45 @@ def test_permutation_and_shard_invariance():
             assert np.array_equal(np.concatenate([q[k] for q in parts]), a[k])
 
 
-def test_host_entry_point_matches_device_path():
+def _host_buffers(a, dtype, transport):
+    """CPU tensors for the host entry point: pinned (zero-copy transport),
+    pageable (staged), or pinned inputs with pageable outputs (staged)."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.pin_memory() if transport in ("zero_copy", "forced_staged") else t
+
+
+@pytest.mark.parametrize("transport", ["zero_copy", "staged_pageable", "staged_mixed", "forced_staged"])
+def test_host_entry_point_matches_device_path(transport, monkeypatch):
+    """Both transports of bessel_logk_f64_host (zero-copy for mapped pinned
+    buffers, staged chunks otherwise) equal the device path bit for bit, with
+    a ragged last chunk; one output NULL on the zero-copy transport too."""
+    if transport == "forced_staged":
+        monkeypatch.setenv("BLK_HOST_PIPELINE", "1")
     v, x = workloads.generate("c2", 0, 70001)
     dev = run_gpu(v, x, lanes_per_element=1)
-    vt = torch.from_numpy(v).pin_memory()
-    xt = torch.from_numpy(x).pin_memory()
-    outs = [torch.empty(v.size, dtype=torch.float64).pin_memory() for _ in range(3)]
+    vt = _host_buffers(v, torch.float64, "zero_copy" if transport == "staged_mixed" else transport)
+    xt = _host_buffers(x, torch.float64, "zero_copy" if transport == "staged_mixed" else transport)
+    outs = [_host_buffers(np.full(v.size, np.nan), torch.float64, transport) for _ in range(3)]
     chunk = 16384
     ws = torch.empty(blk.host_workspace_bytes(chunk), dtype=torch.uint8, device=DEV)
     blk.bessel_logk_f64_host(vt, xt, *outs, nbins=NB, workspace=ws, chunk=chunk)
     for k, o in zip(KINDS, outs):
         assert np.array_equal(o.numpy(), dev[k]), k
+    # dlogk_dv NULL: the other two outputs unchanged, nothing written for dv
+    outs2 = [_host_buffers(np.full(v.size, np.nan), torch.float64, transport) for _ in range(3)]
+    blk.bessel_logk_f64_host(vt, xt, outs2[0], None, outs2[2], nbins=NB, workspace=ws, chunk=chunk)
+    assert np.array_equal(outs2[0].numpy(), dev["logk"])
+    assert np.array_equal(outs2[2].numpy(), dev["dx"])
+    assert np.all(np.isnan(outs2[1].numpy()))
 
 
-def test_host_entry_point_f32_matches_device_path():
+@pytest.mark.parametrize("transport", ["zero_copy", "staged_pageable"])
+def test_host_entry_point_f32_matches_device_path(transport):
     v, x = workloads.generate("c4", 0, 50003)
     dev = run_gpu(v, x, lanes_per_element=1)
-    vt = torch.from_numpy(v).pin_memory()
-    xt = torch.from_numpy(x).pin_memory()
-    outs = [torch.empty(v.size, dtype=torch.float32).pin_memory() for _ in range(3)]
+    vt = _host_buffers(v, torch.float32, transport)
+    xt = _host_buffers(x, torch.float32, transport)
+    outs = [_host_buffers(np.zeros(v.size, np.float32), torch.float32, transport) for _ in range(3)]
     chunk = 8192
     ws = torch.empty(blk.host_workspace_bytes(chunk, 4), dtype=torch.uint8, device=DEV)
     blk.bessel_logk_f32_host(vt, xt, *outs, nbins=NB, workspace=ws, chunk=chunk)
