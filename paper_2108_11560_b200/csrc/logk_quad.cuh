@@ -50,6 +50,10 @@ constexpr int kGroup2 = BLK_GROUP2; // v2 loop group size
 #define BLK_V2_UNROLL 1
 #endif
 constexpr int kV2Unroll = BLK_V2_UNROLL; // tuning knob: unroll of the v2 group loop
+#ifndef BLK_S1_SPLIT
+#define BLK_S1_SPLIT 1
+#endif
+constexpr bool kS1Split = BLK_S1_SPLIT;   // v2 loop: S1 as t_c sum Ep + h sum j Ep per group
 
 // 2^(j/2048) with (j << 9) subtracted from the high word (gen_exp2_table.py):
 // adding (k << 9) to the high word of entry k & 2047 gives 2^(k/2048) for
@@ -461,7 +465,7 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
   // e^{-2v G h} by squaring: q only enters w = E (1 + q), where a few ulp of
   // drift over n/G steps are far below the other rounding (measured +1%)
   const double eq2 = eq1 * eq1, eqG = eq2 * eq2;
-  double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0;
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0, S1j = 0.0;
   if (ib == 0) {
     // node 0 carries weight 1/2: take half of it back (exact state)
     const double X = XpG + XmG;
@@ -498,11 +502,29 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
     for (int j = 0; j < G; ++j) ts[j] = exp_scale(k[j]);
 #pragma unroll
     for (int j = 0; j < G; ++j) r[j] = fma(kd[j], kNegExpCc, a[j]);
+    if (HESS || !DV || !kS1Split) {
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
-      v2_accumulate<DV, DX, HESS>(E, q[j], X[j], j == 0 ? tc : fma(double(j), h, tc), S0, S1,
-                                  S2, S11, S22, S12);
+      for (int j = 0; j < G; ++j) {
+        const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
+        v2_accumulate<DV, DX, HESS>(E, q[j], X[j], j == 0 ? tc : fma(double(j), h, tc), S0,
+                                    S1, S2, S11, S22, S12);
+      }
+    } else {
+      // S1 = sum Ep_j (t_c + j h) = t_c sum Ep_j + h sum j Ep_j: per group one
+      // three-register FMA instead of four (Ep = E (1 - q) >= 0, no cancellation)
+      double Ep[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const double E = fma(ts[j], exp_em1(r[j]), ts[j]);
+        const double w = fma(E, q[j], E);
+        S0 += w;
+        if (DX) S2 = fma(w, X[j], S2);
+        Ep[j] = fma(E, 2.0, -w);
+      }
+      static_assert(G == 4, "S1 split below is written for groups of 4");
+      const double A = (Ep[0] + Ep[1]) + (Ep[2] + Ep[3]);
+      S1 = fma(tc, A, S1);
+      S1j += fma(Ep[3], 3.0, fma(Ep[2], 2.0, Ep[1]));
     }
   }
   double xp = XpG, xm = XmG, qq = qG;
@@ -517,7 +539,7 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
   }
   const double rx = rcp64(x);
   out.S0 += S0;
-  if (DV || HESS) out.S1 += S1;
+  if (DV || HESS) out.S1 += fma(h, S1j, S1);
   if (DX || HESS) out.S2 += S2 * rx;
   if (HESS) {
     out.S11 += S11;
