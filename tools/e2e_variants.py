@@ -3,6 +3,9 @@ import ctypes
 import os
 import sys
 
+# chunked (staged) transport: pinned buffers would otherwise take the zero-copy one
+os.environ["BLK_HOST_PIPELINE"] = "1"
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
