@@ -73,7 +73,9 @@ typedef enum {
 
 /* Range-finding precision (options.range_mode). */
 #define BLK_RANGE_AUTO 0  /* FP32 (FMA + MUFU pipes) inside its safe domain, else FP64 */
-#define BLK_RANGE_F64 1   /* working-precision range finding, as the paper does */
+#define BLK_RANGE_F64 1   /* working-precision range finding, as the paper does: FP64,
+                             FindZero until the Newton step is below 2^-45 of the
+                             scale (the oracle's fixed-10-iteration ranges) */
 
 typedef struct {
     /* Lanes cooperating on one element (1 = one element per thread; 2..32,
