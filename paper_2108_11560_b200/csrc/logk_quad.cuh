@@ -39,7 +39,10 @@ constexpr int kAnchor = BLK_ANCHOR; // v1 loop: FP64 re-anchoring interval for e
 #define BLK_GROUP 4
 #endif
 #ifndef BLK_MINB
-#define BLK_MINB 6
+// __launch_bounds__ min blocks per SM: 5 lets ptxas use 90 registers (6 capped
+// it at 78 and cost the session-3 loop 2-2.5%; 4 measures the same as 5 on
+// c2/c3/c5, profiles/r01s3g_minb_sweep.log)
+#define BLK_MINB 5
 #endif
 constexpr int kGroup = BLK_GROUP; // nodes evaluated together (independent exp chains)
 #ifndef BLK_GROUP2
