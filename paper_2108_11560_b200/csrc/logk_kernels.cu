@@ -194,8 +194,13 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   if (dvx_out) dvx_out[i] = ok ? sgn * fma(m1, m2, -(s.S12 * r)) : nanv;
 }
 
+#ifndef BLK_F32_MINB
+// FP32 entry point: 6 resident blocks per SM (ptxas then fits 80 registers;
+// unconstrained it took 96 and ran 5): c4 +3.2% (profiles/r01s3h_f32_minb.log)
+#define BLK_F32_MINB 6
+#endif
 template <bool LOGK, bool DV, bool DX, int LPE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, BLK_F32_MINB)
 logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, size_t n_el,
                 float *__restrict__ logk, float *__restrict__ dlogk_dv,
                 float *__restrict__ dlogk_dx, int nbins, int range_mode) {
