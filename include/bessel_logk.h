@@ -72,7 +72,10 @@ typedef enum {
 #define BLK_MAX_NBINS 65536
 
 /* Range-finding precision (options.range_mode). */
-#define BLK_RANGE_AUTO 0  /* FP32 (FMA + MUFU pipes) inside its safe domain, else FP64 */
+#define BLK_RANGE_AUTO 0  /* FP32 (FMA + MUFU pipes) when nbins >= 64 and the element is
+                             inside the FP32-safe domain (x in [1e-30, 1e4], |v| <= 1e4),
+                             else FP64 as below: coarse grids are sensitive to the
+                             node placement (R20) */
 #define BLK_RANGE_F64 1   /* working-precision range finding, as the paper does: FP64,
                              FindZero until the Newton step is below 2^-45 of the
                              scale (the oracle's fixed-10-iteration ranges) */
@@ -87,18 +90,16 @@ typedef struct {
     /* Threads per block of the simple kernel (0 = default 128; else a
      * multiple of 32 in [32, 128]). */
     int block_threads;
-    /* Kernel variant: BLK_KERNEL_AUTO (= BLK_KERNEL_SIMPLE),
-     * BLK_KERNEL_SIMPLE (one element -- or lanes_per_element lanes -- per
-     * thread, both phases in every warp), BLK_KERNEL_WS (FP64 only,
-     * persistent: producer warps find the ranges, consumer warps integrate;
-     * one element per lane).  Every variant gives bit-identical results for
-     * lanes_per_element = 1. */
+    /* Kernel variant: BLK_KERNEL_AUTO or BLK_KERNEL_SIMPLE (the same
+     * kernel: one element -- or lanes_per_element lanes -- per thread, both
+     * phases in every warp).  Any other value is BLK_EINVAL.  (A
+     * warp-specialised producer/consumer variant was measured 10-20% slower
+     * and removed.) */
     int kernel;
 } blk_options;
 
 #define BLK_KERNEL_AUTO 0
 #define BLK_KERNEL_SIMPLE 1
-#define BLK_KERNEL_WS 2
 
 /*
  * FP64 entry point.  eps = 2^-52 (log eps = -36.0437, R9).
@@ -132,7 +133,7 @@ BLK_API blk_status bessel_logk_f32_ex(const float *v, const float *x, size_t n,
  *    cudaHostRegister under unified addressing -- e.g. torch pin_memory), one
  *    kernel launch reads the inputs and writes the outputs over PCIe
  *    directly, so the transfers overlap the computation element by element
- *    (the workspace is not touched);
+ *    (the workspace is not used and may be NULL);
  *  - staged: otherwise (pageable memory works but serialises), the batch is
  *    split into chunks of `chunk` elements (0 = default 2^20) that are copied
  *    host->device, computed and copied device->host on a small pool of
@@ -140,7 +141,8 @@ BLK_API blk_status bessel_logk_f32_ex(const float *v, const float *x, size_t n,
  *    (BLK_HOST_PIPELINE=1 in the environment forces this path; measurement
  *    only.)
  * workspace: DEVICE buffer of at least bessel_logk_host_workspace_bytes(chunk,
- * 8) bytes, owned by the caller (required on both transports).
+ * 8) bytes, owned by the caller; required (BLK_EINVAL if NULL or too small)
+ * only when the staged transport is taken.
  * Blocking: returns after all results are in host memory (the work is ordered
  * after prior work on `stream`).  Both transports run the simple kernel with
  * one element per lane, so results equal bessel_logk_f64_ex with
@@ -157,18 +159,6 @@ BLK_API blk_status bessel_logk_f32_host(const float *v, const float *x, size_t n
                                 float *logk, float *dlogk_dv, float *dlogk_dx,
                                 int nbins, void *workspace, size_t workspace_bytes,
                                 size_t chunk, cudaStream_t stream);
-
-/*
- * Diagnostic entry point: the FP64 hot path as two kernels -- `phases` bit 0
- * runs the range finding for all elements into `scratch` (DEVICE, 32 bytes
- * per element, caller-owned), bit 1 the quadrature + epilogue from it.  All
- * three outputs are required.  Results equal bessel_logk_f64 bit for bit; it
- * exists to time the two phases separately (tools/, profiles/).
- */
-BLK_API blk_status blk_debug_split_f64(const double *v, const double *x, size_t n,
-                                       double *logk, double *dlogk_dv, double *dlogk_dx,
-                                       int nbins, void *scratch, int phases,
-                                       cudaStream_t stream);
 
 /*
  * Second derivatives in the same pass: from the

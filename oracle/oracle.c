@@ -22,8 +22,10 @@
  * K_{v+1}=K_{v-1}+(2v/x)K_v, symmetry in v, the identity
  * Eq. (deriv), d/dv = 0 at v = 0, mpmath besselk, and the
  * independent long-double brute force in oracle/brute.c.  The plan internals
- * (t_p, t0, t1) are "parity unpinned" by design (R20): only their sign
- * invariants are asserted.
+ * (t_p, t0, t1) are pinned to 30-digit roots of g' = 0 and d(t) = 0
+ * (tests/test_oracle_pins.py::test_plan_vs_mpmath_roots): each lies on the
+ * outer side of its root (R1) within the 10-iteration bracket bound W0 2^-10,
+ * and a FindZero that stalls (0, 1 or 3 iterations) fails that pin.
  */
 #include <math.h>
 #include <stddef.h>
@@ -104,7 +106,8 @@ static int find_range(const oracle_ctx *c, ofun F, double ts, double *lo, double
  * R1 (F(a) < 0 <= F(b), a is the end Alg. 3 passes first, return a),
  * R2 (Newton from the current a), R3 (clip to the segment [a, mid]),
  * R4 (max_iter = 10 fixed iterations when tol <= 0; tol > 0 reproduces the
- *     literal early exit "until |a_i - a_{i-1}| < tol"),
+ *     literal early exit "until |a_i - a_{i-1}| < tol"; max_iter = 0 returns
+ *     the start a -- only for the negative pin of the plan test),
  * R18 (F'(a) == 0 or non-finite Newton step -> use the bisection point).
  */
 static double find_zero(const oracle_ctx *c, ofun F, ofun dF, double a, double b,
@@ -316,7 +319,7 @@ int oracle_logk(const double *v, const double *x, size_t n,
                 int nbins, int max_iter, double tol, double log_eps,
                 double *plan)
 {
-    if (nbins < 1 || max_iter < 1)
+    if (nbins < 1 || max_iter < 0)   /* max_iter = 0: FindZero returns its start (negative pin) */
         return -1;
     for (size_t i = 0; i < n; ++i) {
         double a, b, d;

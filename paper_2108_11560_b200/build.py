@@ -62,6 +62,17 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     return target
 
 
+def build_diag() -> str:
+    """The diagnostics variant (tools/ only; -DBLK_DIAG adds the two-kernel
+    split blk_debug_split_f64, not part of the public ABI):
+    paper_2108_11560_b200/variants/diag.so."""
+    out = os.path.join(HERE, "variants", "diag.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    if os.path.exists(out) and all(os.path.getmtime(d) <= os.path.getmtime(out) for d in _deps()):
+        return out
+    return build(out=out, defines=["BLK_DIAG"])
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

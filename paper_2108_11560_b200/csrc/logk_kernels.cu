@@ -19,16 +19,14 @@
 #include "../../include/bessel_logk.h"
 #include "logk_quad.cuh"
 #include "logk_range.cuh"
-#include "logk_ws.cuh"
-#include "logk_split.cuh"
 #include "logk_nig.cuh"
+#ifdef BLK_DIAG
+#include "logk_split.cuh"   // diagnostics build only (tools/): the two phases as two kernels
+#endif
 
 namespace blk {
 
 constexpr int kDefaultThreads = 128;
-#ifndef BLK_F32_NEWTON
-#define BLK_F32_NEWTON false  // FP32 entry point plan: 1/(1+q) by MUFU.RCP (Newton steps on the FMA pipe measured no faster)
-#endif
 
 #ifdef BLK_TIMELINE
 // Diagnostic build only (tools/build_variants.py ...=BLK_TIMELINE): per-warp
@@ -99,7 +97,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
   bool ok = false;
   if (valid) {
-    if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
+    if (use_f32_plan(range_mode, nbins, v, x)) {
       const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
                                        : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
@@ -160,7 +158,7 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
   bool ok = false;
   if (valid) {
-    if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
+    if (use_f32_plan(range_mode, nbins, v, x)) {
       const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
                                        : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
@@ -217,10 +215,10 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   float t0 = 0.0f, t1 = 0.0f, gp = 0.0f, dmin = 0.0f;
   bool ok = false;
   if (valid) {
-    if (range_mode == BLK_RANGE_AUTO && f32_plan_domain(v, x)) {
+    if (use_f32_plan(range_mode, nbins, v, x)) {
       const Plan<float> p =
-          (LPE >= 2) ? make_plan_f32_pair<BLK_F32_NEWTON>(v, x, kLogEpsF32, fz_tol_for(nbins), sub & 1)
-                     : make_plan_f32<BLK_F32_NEWTON>(v, x, kLogEpsF32, fz_tol_for(nbins));
+          (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF32, fz_tol_for(nbins), sub & 1)
+                     : make_plan_f32(v, x, kLogEpsF32, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);
@@ -351,9 +349,7 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
     kernel = opts->kernel;
     if (opts->block_threads) threads = opts->block_threads;
   }
-  if (kernel < BLK_KERNEL_AUTO || kernel > BLK_KERNEL_WS) return fail(BLK_EINVAL, "bad kernel variant");
-  if (kernel == BLK_KERNEL_WS && lanes > 1) return fail(BLK_EINVAL, "the warp-specialized kernel has one element per lane");
-  if (kernel == BLK_KERNEL_WS && sizeof(T) != 8) return fail(BLK_EINVAL, "the warp-specialized kernel is FP64 only");
+  if (kernel != BLK_KERNEL_AUTO && kernel != BLK_KERNEL_SIMPLE) return fail(BLK_EINVAL, "bad kernel variant");
   if (nbins < 2 || nbins > BLK_MAX_NBINS) return fail(BLK_EINVAL, "nbins out of range [2, 65536]");
   if (n > 0 && !o1 && !o2 && !o3) return fail(BLK_EINVAL, "all outputs are NULL");
   if (n > 0 && (!v || !x)) return fail(BLK_EINVAL, "v or x is NULL");
@@ -361,11 +357,8 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
   if (lanes < 0 || lanes > 32 || (lanes & (lanes - 1))) return fail(BLK_EINVAL, "lanes_per_element must be 0 or a power of two <= 32");
   if (threads < 32 || threads > 128 || threads % 32) return fail(BLK_EINVAL, "block_threads must be a multiple of 32 in [32, 128]");
   if (n > ((size_t)1 << 40)) return fail(BLK_EINVAL, "n too large");
-  // The warp-specialized kernel is measured slower on B200 (the path is
-  // issue-bound, so splitting the phases across warps adds nothing; see
-  // DESIGN.md §6): AUTO selects the simple kernel.
-  if (kernel == BLK_KERNEL_AUTO) kernel = BLK_KERNEL_SIMPLE;
-  if (lanes == 0) lanes = (kernel == BLK_KERNEL_WS) ? 1 : auto_lanes(n, nbins);
+  kernel = BLK_KERNEL_SIMPLE;
+  if (lanes == 0) lanes = auto_lanes(n, nbins);
   return BLK_OK;
 }
 
@@ -403,30 +396,6 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
   }
 #endif
 
-template <class K>
-blk_status launch_ws(K kern, size_t n, cudaStream_t st, const double *v, const double *x,
-                     double *a, double *b, double *c, int nbins, int mode) {
-  const size_t smem = sizeof(blk::WsShared);
-  int dev, sms = 0, per_sm = 0;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, blk::kWsThreads, smem);
-  if (e != cudaSuccess) return cuda_fail(e, "ws occupancy query");
-  if (per_sm < 1) return fail(BLK_ECUDA, "ws kernel cannot be resident");
-  const size_t tiles = (n + 31) / 32;
-  size_t grid = (size_t)sms * per_sm;
-  if (grid > tiles) grid = tiles;
-  kern<<<(unsigned)grid, blk::kWsThreads, smem, st>>>(v, x, n, a, b, c, nbins, mode);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "ws kernel launch");
-  return BLK_OK;
-}
-
-#define BLK_WS(O1, O2, O3) \
-  return launch_ws(blk::logk_f64_ws_kernel<O1, O2, O3>, n, stream, v, x, a, b, c, nbins, mode);
-
 template <class T>
 blk_status run(const T *v, const T *x, size_t n, T *a, T *b, T *c, int nbins,
                const blk_options *opts, cudaStream_t stream) {
@@ -436,17 +405,6 @@ blk_status run(const T *v, const T *x, size_t n, T *a, T *b, T *c, int nbins,
   if (n == 0) return BLK_OK;
   const int sel = (a ? 4 : 0) | (b ? 2 : 0) | (c ? 1 : 0);
   if constexpr (sizeof(T) == 8) {
-    if (kernel == BLK_KERNEL_WS) {
-      switch (sel) {
-        case 7: BLK_WS(true, true, true)
-        case 6: BLK_WS(true, true, false)
-        case 5: BLK_WS(true, false, true)
-        case 4: BLK_WS(true, false, false)
-        case 3: BLK_WS(false, true, true)
-        case 2: BLK_WS(false, true, false)
-        default: BLK_WS(false, false, true)
-      }
-    }
     switch (sel) {
       case 7: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, true, true)
       case 6: BLK_DISPATCH_LPE(blk::logk_f64_kernel, lanes, true, true, false)
@@ -548,8 +506,6 @@ blk_status run_host(const T *v, const T *x, size_t n, T *logk, T *dlogk_dv, T *d
   if (st != BLK_OK) return st;
   if (n == 0) return BLK_OK;
   if (chunk == 0) chunk = (size_t)1 << 20;
-  if (!workspace || workspace_bytes < bessel_logk_host_workspace_bytes(chunk, sizeof(T)))
-    return fail(BLK_EINVAL, "workspace missing or too small");
   // Zero-copy: when every buffer is page-locked host memory mapped into the
   // device address space (cudaHostAlloc / cudaHostRegister under UVA, e.g.
   // torch's pin_memory), one launch reads the inputs and writes the outputs
@@ -579,6 +535,9 @@ blk_status run_host(const T *v, const T *x, size_t n, T *logk, T *dlogk_dv, T *d
       }
     }
   }
+  // staged transport: the device workspace holds the chunks in flight
+  if (!workspace || workspace_bytes < bessel_logk_host_workspace_bytes(chunk, sizeof(T)))
+    return fail(BLK_EINVAL, "workspace missing or too small (staged transport)");
   Pool *pool;
   st = get_pool(pool);
   if (st != BLK_OK) return st;
@@ -681,7 +640,6 @@ blk_status bessel_logk_hess_f64(const double *v, const double *x, size_t n, doub
   blk_status st = validate(v, x, n, any ? (void *)1 : nullptr, nullptr, nullptr, nbins, opts,
                            lanes, mode, th, kernel);
   if (st != BLK_OK) return st;
-  if (kernel == BLK_KERNEL_WS) return fail(BLK_EINVAL, "no warp-specialized Hessian kernel");
   if (n == 0) return BLK_OK;
   const size_t total = n * (size_t)lanes;
   const size_t blocks = (total + th - 1) / th;
@@ -702,7 +660,11 @@ blk_status bessel_logk_hess_f64(const double *v, const double *x, size_t n, doub
   return e == cudaSuccess ? BLK_OK : cuda_fail(e, "hess kernel launch");
 }
 
-blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, double *logk,
+#ifdef BLK_DIAG
+// Diagnostics build only (tools/phase_split.py etc.; not in the public header):
+// the FP64 path as two kernels, plan into `scratch` (32 B per element), then
+// quadrature + epilogue, to time the phases separately.
+__attribute__((visibility("default"))) blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, double *logk,
                                double *dlogk_dv, double *dlogk_dx, int nbins, void *scratch,
                                int phases, cudaStream_t s) {
   if (!v || !x || !logk || !dlogk_dv || !dlogk_dx || !scratch || nbins < 2 || nbins > BLK_MAX_NBINS)
@@ -717,6 +679,7 @@ blk_status blk_debug_split_f64(const double *v, const double *x, size_t n, doubl
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BLK_OK : cuda_fail(e, "split kernels");
 }
+#endif
 
 #ifdef BLK_TIMELINE
 __attribute__((visibility("default"))) blk_status blk_debug_timeline(unsigned long long *host, size_t max_warps) {

@@ -48,7 +48,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
     if (z > 0.0 && isfinite(z)) {
       double t0, t1, gp, dmin;
       bool ok;
-      if (f32_plan_domain(1.0, z)) {
+      if (use_f32_plan(0, nbins, 1.0, z)) {
         const Plan<float> p = make_plan_f32(1.0, z, kLogEpsF64, fz_tol_for(nbins));
         ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
       } else {

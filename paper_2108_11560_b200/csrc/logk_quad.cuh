@@ -580,7 +580,8 @@ __device__ __forceinline__ void end_half_f32(double v, double x, double s_mid, d
 // Nodes [mb, me) of the n-interval trapezoid on [t0, t0 + n h] (node m at
 // t0 + m h; nodes 0 and n carry weight 1/2: all nodes are summed
 // with weight 1 and half of each end node is taken back).  The lane owning
-// node 0 has mb == 0, the lane owning node n has me == n + 1.
+// node 0 has mb == 0, the lane owning node n has mb < me == n + 1 (lanes past
+// the last node get the empty range mb == me == n + 1 and take nothing back).
 template <bool DV, bool DX, bool CLAMP, bool HESS = false>
 __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double h,
                                            double shift, int n, int mb, int me,
@@ -596,7 +597,7 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
     nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, s);
   // node n: t_n = t1 lies outside the eps-support (d(t1) < 0, FindZero
   // returns the outer end, R1), so its term is < 2^-52 of the peak term
-  if (me == n + 1) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
+  if (mb < me && me == n + 1) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
   return s;
 }
 
@@ -606,29 +607,6 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
 struct Sums32 {
   double S0, S1, S2;
 };
-
-// exp(a) with the argument split so that ex2.approx sees an exactly
-// representable a*log2(e) (hi) and the rounding residue (lo) is applied to
-// first order: relative error ~2 ulp instead of |a| ulp.
-__device__ __forceinline__ float exp_split_f32(float a) {
-  const float kL2e = 1.4426950408889634f;
-  const float kL2eLo = 1.9259629911266175e-08f;       // log2(e) - kL2e
-  float y = a * kL2e;
-  float yl = fmaf(a, kL2e, -y);
-  yl = fmaf(a, kL2eLo, yl);
-  float e = ex2_approx(y);
-  return fmaf(e, yl * 0.6931471805599453f, e);
-}
-
-// 1/a for a in a normal range without MUFU: magic-constant seed (12%) and
-// three Newton steps (-> ~1 ulp).  Used where the kernel is MUFU-bound.
-__device__ __forceinline__ float2 rcp_newton2(float2 a) {
-  float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(a.x)),
-                         __int_as_float(0x7EF311C3 - __float_as_int(a.y)));
-#pragma unroll
-  for (int i = 0; i < 3; ++i) y = mul2(y, fma2(mul2(a, f2s(-1.0f)), y, f2s(2.0f)));
-  return y;
-}
 
 // FP32 entry point quadrature.  The weight exponent g(t) - s is a difference
 // of terms as large as v t and x cosh t (~1e2 in config 4) whose FP32
@@ -746,7 +724,7 @@ __device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float 
     if (DV) S1 -= double(E * tf) * (-expm1f(-2.0f * vf * tf));
   };
   if (mb == 0) half_node(0);
-  if (me == n + 1) half_node(n);
+  if (mb < me && me == n + 1) half_node(n);
   return Sums32{S0, S1, S2};
 }
 
@@ -887,7 +865,7 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
     if (DV) S1 -= double(E * tf1) * (-expm1f(-2.0f * vf * tf1));
   };
   if (mb == 0) half_node(0, hx2 * (ebx + rcp64(ebx)));
-  if (me == n + 1) half_node(n, fma(XpG, e1i, XmG * e1));
+  if (mb < me && me == n + 1) half_node(n, fma(XpG, e1i, XmG * e1));
   return Sums32{S0, S1, S2};
 }
 

@@ -64,33 +64,8 @@ struct Plan {
   bool ok;
 };
 
-// 1/(1+q) for q in [0,1] without MUFU: linear seed on [1,2] (max error 6%)
-// and three Newton steps (6e-8).  Used by the FP32 entry point, whose range
-// finding is MUFU-bound; the FP64 kernel is issue-bound and keeps MUFU.RCP.
-__device__ __forceinline__ float2 rcp_1pq2(float2 opq) {
-  float2 r = fma2(opq, f2s(-0.5f), f2s(1.4571f));
-#pragma unroll
-  for (int i = 0; i < 3; ++i) r = mul2(r, fma2(mul2(opq, f2s(-1.0f)), r, f2s(2.0f)));
-  return r;
-}
-
-// e^{-t} = 1/e^t without MUFU: magic-constant seed, three Newton steps; e^t
-// beyond 2^120 (t > 83, only FindRange probes get there) maps to 0.
-// (Measured slower than MUFU.RCP in the FP32 kernel -- it turns it
-// issue-bound -- so it is not used; kept for reference.)
-__device__ __forceinline__ float2 rcp_exp2(float2 e) {
-  float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(e.x)),
-                         __int_as_float(0x7EF311C3 - __float_as_int(e.y)));
-#pragma unroll
-  for (int i = 0; i < 3; ++i) y = mul2(y, fma2(mul2(e, f2s(-1.0f)), y, f2s(2.0f)));
-  y.x = e.x > 1.3e36f ? 0.0f : y.x;
-  y.y = e.y > 1.3e36f ? 0.0f : y.y;
-  return y;
-}
-
 // ============================================================== FP32 (packed)
-template <bool NEWTON>
-struct PlanF32T {
+struct PlanF32 {
   static constexpr float kL2e = 1.4426950408889634f;
   static constexpr float kLn2f = 0.6931471805599453f;
   float v, x, hx, v2, m2vs, L;
@@ -107,7 +82,7 @@ struct PlanF32T {
     float2 e = ex2_2(mul2(t, f2s(kL2e)));
     float2 ei = rcp_2(e);
     float2 q = ex2_2(mul2(t, f2s(m2vs)));
-    float2 r = NEWTON ? rcp_1pq2(add2(q, f2s(1.0f))) : rcp_2(add2(q, f2s(1.0f)));
+    float2 r = rcp_2(add2(q, f2s(1.0f)));
     float2 th = mul2(add2(f2s(1.0f), mul2(q, f2s(-1.0f))), r);
     float2 s2 = mul2(mul2(q, f2s(4.0f)), mul2(r, r));
     F = fma2(f2s(v), th, mul2(f2s(-hx), add2(e, mul2(ei, f2s(-1.0f)))));
@@ -126,7 +101,7 @@ struct PlanF32T {
     float2 ei = rcp_2(e);
     float2 q = ex2_2(mul2(t, f2s(m2vs)));
     float2 opq = add2(q, f2s(1.0f));
-    float2 r = NEWTON ? rcp_1pq2(opq) : rcp_2(opq);
+    float2 r = rcp_2(opq);
     float2 lq = lg2_2(opq);
     float2 base = fma2(lq, f2s(kLn2f), f2s(-c));
     base = fma2(f2s(v), t, base);
@@ -181,8 +156,6 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
   a = na; Fa = nFa; dFa = ndFa;
 }
 
-using PlanF32 = PlanF32T<false>;
-
 // Alg. 2 with the two evaluations packed into f32x2 operations.  The loop
 // ends after max_iter = 10 iterations or earlier, per the paper's
 // "until" clause, once the Newton correction from the kept end a is
@@ -192,14 +165,13 @@ using PlanF32 = PlanF32T<false>;
 // which changes no output beyond rounding (R4, R20).  The literal
 // tol = 1 on |a_i - a_{i-1}| is not used (R4: it stops on the first
 // iteration that keeps a, and breaks config 3).
-// The tolerance follows the grid: from nbins = 128 the trapezoid error is at
-// rounding level and insensitive to the range (R20), so 2^-8 (the range is
-// then at most ~0.4% of its half-width wider than converged); 64-127 bins can
-// still carry a discretisation error on extreme inputs that a wider range
-// shifts, so 2^-10; coarser grids are sensitive to where the nodes fall, so
-// 2^-20 (FP32 resolution), and there the peak is found to that resolution too.
+// The tolerance follows the grid (the FP32 finder only runs from 64 bins on,
+// kF32PlanMinBins): from nbins = 128 the trapezoid error is at rounding level
+// and insensitive to the range (R20), so 2^-8 (the range is then at most
+// ~0.4% of its half-width wider than converged); 64-127 bins can still carry
+// a discretisation error on extreme inputs that a wider range shifts, so 2^-10.
 __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
-  return nbins >= 128 ? 3.90625e-3f : (nbins >= 64 ? 9.765625e-4f : 9.5367431640625e-7f);
+  return nbins >= 128 ? 3.90625e-3f : 9.765625e-4f;
 }
 // For the PEAK search (F = g', F' = g'') what matters is not where t_p is
 // but how far g(a) lies below the maximum, because g(t_p) becomes the
@@ -221,8 +193,7 @@ __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, fl
     // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
     // carries no information and must not end the search)
     if (PEAK && tol >= 3e-3f) {
-      // (on coarse grids, tol = 2^-20, the peak too is found to FP32
-      // resolution: there the nodes' placement matters, see fz_tol_for)
+      // (at 64-127 bins, tol = 2^-10, the peak is found like the range ends)
       if (Fa * Fa <= (2.0f * kPeakGapTol) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
     } else {
       const float rhs = tol * fabsf((a - ref) * dFa);
@@ -259,13 +230,12 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 
 // Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
 // is taken in double on the caller's inputs.
-template <bool NEWTON = false>
 __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps,
                                                     float tol) {
   Plan<float> p;
-  PlanF32T<NEWTON> P;
+  PlanF32 P;
   P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
-  P.m2vs = -2.0f * P.v * PlanF32T<NEWTON>::kL2e; P.L = float(log_eps);
+  P.m2vs = -2.0f * P.v * PlanF32::kL2e; P.L = float(log_eps);
   float lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0f;
@@ -317,13 +287,12 @@ __device__ __forceinline__ float find_zero_f32_rt(const PF &P, float c, float a,
 // shuffle.  Same ranges as make_plan_f32 (the same arithmetic per search);
 // the latency of one of the two searches is saved, which is what bounds
 // small batches.  All lanes of the pair must be active.
-template <bool NEWTON = false>
 __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, double log_eps,
                                                          float tol, bool odd) {
   Plan<float> p;
-  PlanF32T<NEWTON> P;
+  PlanF32 P;
   P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
-  P.m2vs = -2.0f * P.v * PlanF32T<NEWTON>::kL2e; P.L = float(log_eps);
+  P.m2vs = -2.0f * P.v * PlanF32::kL2e; P.L = float(log_eps);
   float lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0f;
@@ -442,6 +411,17 @@ __device__ __forceinline__ Plan<double> make_plan_f64(double v, double x, double
 // error stays below ~0.1 in log units.
 __device__ __forceinline__ bool f32_plan_domain(double v, double x) {
   return x >= 1e-30 && x <= 1e4 && v <= 1e4;
+}
+
+// Below this many bins BLK_RANGE_AUTO also takes the FP64 range finder: a
+// coarse grid's discretisation error depends on where the nodes fall, so
+// only the paper's working-precision ranges reproduce the oracle there
+// (R20); from it on the result is insensitive to the range.
+constexpr int kF32PlanMinBins = 64;
+
+// The range finder BLK_RANGE_AUTO picks for one element.
+__device__ __forceinline__ bool use_f32_plan(int range_mode, int nbins, double v, double x) {
+  return range_mode == 0 && nbins >= kF32PlanMinBins && f32_plan_domain(v, x);
 }
 
 }  // namespace blk

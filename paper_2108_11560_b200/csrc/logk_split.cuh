@@ -1,7 +1,8 @@
-// logk_split.cuh -- the hot path as two kernels (plan, then quadrature) with
-// the per-element plan in a caller-provided scratch array.  Used to measure
-// the two phases separately (blk_debug_split_f64) and as the reference point
-// for the fused variants' overlap.
+// logk_split.cuh -- DIAGNOSTICS BUILD ONLY (-DBLK_DIAG, tools/): the hot path
+// as two kernels (plan, then quadrature) with the per-element plan in a
+// caller-provided scratch array, to time the two phases separately
+// (blk_debug_split_f64).  Same range finders as the fused kernel (FP32, or the
+// table-exp FP64 one outside the FP32 domain), so results equal it bit for bit.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -20,6 +21,8 @@ __global__ void __launch_bounds__(128)
 plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 PlanRec *__restrict__ plans, int nbins, int range_mode) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  load_exp_table();   // for make_plan_f64_tab, before any thread leaves
+  __syncthreads();
   if (i >= n_el) return;
   const double vraw = vin[i], x = xin[i];
   const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
@@ -27,11 +30,11 @@ plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
   bool ok = false;
   if (valid) {
-    if (range_mode == 0 && f32_plan_domain(v, x)) {
+    if (use_f32_plan(range_mode, nbins, v, x)) {
       const Plan<float> p = make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
-      const Plan<double> p = make_plan_f64(v, x, kLogEpsF64);
+      const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     }
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;

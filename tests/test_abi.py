@@ -21,7 +21,7 @@ def L():
 
 def test_exports_every_header_function(L):
     names = blk.header_functions()
-    assert len(names) == 16, names
+    assert len(names) == 15, names
     for nm in names:
         assert hasattr(L, nm), nm
     out = subprocess.run(["nm", "-D", "--defined-only", blk.library_path],
@@ -65,11 +65,12 @@ def test_invalid_arguments(L):
     assert _f64(L, FAKE, None, 10, FAKE, None, None, 128) == blk.BLK_EINVAL
     assert b"nbins" in L.bessel_logk_last_error() or L.bessel_logk_last_error()
     bad = [blk._Options(3, 0, 0), blk._Options(64, 0, 0), blk._Options(0, 2, 0),
-           blk._Options(0, 0, 48), blk._Options(0, 0, 256), blk._Options(-1, 0, 0)]
+           blk._Options(0, 0, 48), blk._Options(0, 0, 256), blk._Options(-1, 0, 0),
+           blk._Options(0, 0, 0, 2), blk._Options(0, 0, 0, -1)]
     for o in bad:
         assert _f64(L, FAKE, FAKE, 10, FAKE, None, None, 128, o) == blk.BLK_EINVAL
     assert L.bessel_logk_f32(FAKE, FAKE, 10, None, None, None, 128, None) == blk.BLK_EINVAL
-    assert L.bessel_logk_f64_host(FAKE, FAKE, 10, FAKE, None, None, 128, None, 0, 0,
+    assert L.bessel_logk_f64_host(FAKE, FAKE, 10, FAKE, None, None, 1, None, 0, 0,
                                   None) == blk.BLK_EINVAL
 
 

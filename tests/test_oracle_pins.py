@@ -227,11 +227,32 @@ def test_extreme_domain_vs_brute_force():
     assert rel(o[2], b[2]).max() < 1e-12
 
 
+def test_large_x_dv_vs_brute_force():
+    """d log K/dv for x in [1e5, 1e8] (beyond the configs, R22) against the
+    plain definition.  There every double evaluation of the exponent
+    vt - x cosh t - g(t_p) carries an absolute error ~kappa = eps (x + v t_p
+    + 40) (DESIGN.md §3 tolerance note), which a weighted mean such as
+    S1/S0 turns into a relative error of order kappa; the long double brute
+    force does not (eps_ld x <= 1e-11).  Measured: the oracle within 0.2 kappa
+    (median 0.04 kappa); pinned at 0.5 kappa, the bound the GPU derivative
+    parity tests at large x are stated in."""
+    rng = np.random.default_rng(3)
+    n = 300
+    x = 10 ** rng.uniform(5, 8, n)
+    v = np.where(rng.random(n) < 0.5, rng.uniform(0, 30, n), 10 ** rng.uniform(-3, 3.5, n))
+    lk, dv, dx, plan = oracle.logk(v, x, 128, with_plan=True)
+    b = oracle.brute(v, x, threads=8)
+    kappa = np.finfo(float).eps * (x + v * plan[:, 0] + 40.0)
+    assert np.all(np.abs(dv - b[1]) <= 0.5 * kappa * np.abs(b[1]))
+    assert rel(dx, b[2]).max() < 1e-12
+    assert rel_logk(lk, b[0]).max() < TOL_LOGK
+
+
 # ------------------------------------------------------------ plan invariants
 def test_plan_sign_invariants():
-    """Plan internals are parity-unpinned (R20); assert the sign invariants that
-    define them: g'(t_p) <= 0 (peak approached from outside, R1), d(t0) <= 0 when
-    t0 > 0, d(t1) < 0, t0 <= t_p <= t1."""
+    """The sign invariants that define the plan: g'(t_p) <= 0 (peak approached
+    from outside, R1), d(t0) <= 0 when t0 > 0, d(t1) < 0, t0 <= t_p <= t1
+    (the plan's values themselves are pinned by test_plan_vs_mpmath_roots)."""
     le = oracle.log_eps_f64()
     for cfg in ["c1", "c2", "c3", "c5"]:
         idx = workloads.sample_indices(cfg, 200, seed=5)
@@ -400,3 +421,142 @@ def test_cancellation_band_vs_brute_force():
     assert np.all(e <= tol), ((e / tol).max(), v[np.argmax(e / tol)], x[np.argmax(e / tol)])
     # and the floor is not vacuous: the oracle's error there is not far below it
     assert (e / tol).max() > 0.05
+
+
+# ------------------------------------------------- the plan vs mpmath roots
+_L_MP = None
+
+
+def _mp_root(f, a, b):
+    """Bisection to ~1e-26 relative on a sign change of f over (a, b)."""
+    fa = f(a)
+    assert fa * f(b) < 0
+    tol = mpmath.mpf(10) ** -26
+    while b - a > tol * max(1, abs(a)):
+        m = (a + b) / 2
+        fm = f(m)
+        if fm == 0:
+            return m
+        if (fm > 0) == (fa > 0):
+            a, fa = m, fm
+        else:
+            b = m
+    return (a + b) / 2
+
+
+def _mp_doubling(F, ts):
+    """Alg. 1's bracket width from t_s (reading R5), with the exact
+    F: m = min{m >= 0 : F(t_s + 2^(m+1)) < 0}; width 2 when m = 0, else 2^m."""
+    m = 0
+    while F(ts + mpmath.mpf(2) ** (m + 1)) >= 0:
+        m += 1
+    return 2.0 if m == 0 else float(2 ** m)
+
+
+def mp_plan(v, x):
+    """The exact plan at 30 digits, from the definitions only (P:91-96,
+    P:121-133): t_p* the root of g' = v tanh(vt) - x sinh t (0 when
+    v^2 <= x), t0*, t1* the roots of d(t) = g(t) - g(t_p*) - log eps left and
+    right of it (t0* = 0 when d(0) <= 0 has no root), plus Alg. 1's initial
+    bracket widths W0 of the three searches (2^m, the t0 search: t_p)."""
+    with mpmath.workdps(30):
+        v, x = mpmath.mpf(float(v)), mpmath.mpf(float(x))
+        L = mpmath.log(mpmath.mpf(2) ** -52)
+
+        def g(t):
+            return mpmath.log(mpmath.cosh(v * t)) - x * mpmath.cosh(t)
+
+        def g1(t):
+            return v * mpmath.tanh(v * t) - x * mpmath.sinh(t)
+
+        tp, w_tp = mpmath.mpf(0), 0.0
+        if v * v - x > 0:
+            w_tp = _mp_doubling(g1, mpmath.mpf(0))
+            hi = mpmath.mpf(2)
+            while g1(hi) > 0:
+                hi *= 2
+            tp = _mp_root(g1, hi * mpmath.mpf(10) ** -30, hi)
+        gp = g(tp)
+
+        def d(t):
+            return g(t) - gp - L
+
+        t0 = mpmath.mpf(0)
+        d0 = float(d(mpmath.mpf(0)))
+        if d0 <= 0:
+            t0 = _mp_root(d, mpmath.mpf(0), tp)
+        w_t1 = _mp_doubling(d, tp)
+        hi = tp + 2
+        while d(hi) >= 0:
+            hi = tp + 2 * (hi - tp)
+        t1 = _mp_root(d, tp, hi)
+        return (float(tp), float(t0), float(t1)), (w_tp, float(tp), w_t1), d0
+
+
+def plan_violations(v, x, plan, exact):
+    """Per element, whether the oracle's (t_p, t0, t1) break the pin:
+      * orientation (R1, Alg. 2 keeps F(a) < 0 and returns a): t_p >= t_p*,
+        t0 <= t0*, t1 >= t1* -- the range is conservative;
+      * the 10-iteration bound: every iteration of Alg. 2 at least halves the
+        bracket (t_shrink, and the Newton point clipped to [a, t_shrink]), so
+        |t - t*| <= W0 2^-10 with W0 Alg. 1's bracket (t_p for the t0 search).
+    Slack 1e-12 max(1, t*) for double rounding of F near its zero."""
+    bad = []
+    for i in range(len(v)):
+        (tp_s, t0_s, t1_s), (w_tp, w_t0, w_t1), _ = exact[i]
+        tp, _, t0, t1 = plan[i]
+        out = False
+        for t, ts, w, side in ((tp, tp_s, w_tp, +1), (t0, t0_s, w_t0, -1), (t1, t1_s, w_t1, +1)):
+            slack = 1e-12 * max(1.0, abs(ts))
+            if side * (t - ts) < -slack or abs(t - ts) > w * 2.0 ** -10 + slack:
+                out = True
+        bad.append(out)
+    return np.array(bad)
+
+
+@pytest.fixture(scope="module")
+def plan_samples():
+    """200 seeded samples per config with their exact plans (elements whose
+    d(0) sits within 1e-9 of the threshold are skipped: there the t0 search
+    is taken or not by rounding)."""
+    out = {}
+    for cfg in ["c1", "c2", "c3", "c4", "c5"]:
+        idx = workloads.sample_indices(cfg, 200, seed=21)
+        v, x = workloads.gather(cfg, idx)
+        v = v.astype(np.float64)
+        x = x.astype(np.float64)
+        ex = [mp_plan(a, b) for a, b in zip(v, x)]
+        keep = np.array([abs(e[2]) > 1e-9 for e in ex])
+        out[cfg] = (v[keep], x[keep], [e for e, k in zip(ex, keep) if k])
+    return out
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_plan_vs_mpmath_roots(plan_samples, cfg):
+    """Alg. 1-3's plan (P:136-218) against 30-digit roots of g' = 0 and
+    d(t) = 0: every t_p, t0, t1 lies on the outer side of its root within the
+    bracket bound of 10 FindZero iterations (see plan_violations); g(t_p) is
+    at most the exact peak value and within |g''| (W0 2^-10)^2 / 2 of it."""
+    v, x, ex = plan_samples[cfg]
+    assert v.size >= 190
+    *_, plan = oracle.logk(v, x, with_plan=True)
+    bad = plan_violations(v, x, plan, ex)
+    assert not bad.any(), (np.nonzero(bad)[0][:5], v[bad][:3], x[bad][:3])
+    for i in range(v.size):
+        with mpmath.workdps(30):
+            vv, xx, tps = mpmath.mpf(v[i]), mpmath.mpf(x[i]), mpmath.mpf(ex[i][0][0])
+            gstar = float(mpmath.log(mpmath.cosh(vv * tps)) - xx * mpmath.cosh(tps))
+        assert plan[i, 1] <= gstar + 1e-13 * max(1.0, abs(gstar))
+
+
+@pytest.mark.parametrize("max_iter", [0, 1, 3])
+def test_plan_pin_rejects_stalled_findzero(plan_samples, max_iter):
+    """Negative pin: a FindZero that stalls -- returns Alg. 1's bracket end
+    (0 iterations) or stops after 1 or 3 -- fails test_plan_vs_mpmath_roots on
+    every config.  The value pins cannot see it: with 3 iterations the n = 128
+    outputs agree with the converged ones to <= 2.3e-14 on c1/c2/c3/c5 (the
+    range is only wider); with 0 or 1 they still do on c1 and c5
+    (c2/c3 overflow: g(t_p) then lies too far below the peak)."""
+    for cfg, (v, x, ex) in plan_samples.items():
+        *_, plan = oracle.logk(v, x, with_plan=True, max_iter=max_iter)
+        assert plan_violations(v, x, plan, ex).any(), (cfg, max_iter)

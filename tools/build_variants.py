@@ -15,7 +15,7 @@ os.makedirs(out_dir, exist_ok=True)
 
 def one(spec):
     name, _, defs = spec.partition("=")
-    defines = ["BLK_MIN_INSTANCES"] + [d for d in defs.split(",") if d]
+    defines = ["BLK_MIN_INSTANCES", "BLK_DIAG"] + [d for d in defs.split(",") if d]
     path = os.path.join(out_dir, name + ".so")
     B.build(out=path, defines=defines)
     return path

@@ -30,7 +30,8 @@ def main():
     n = vt.numel()
     o = [torch.empty_like(vt) for _ in range(3)]
     scratch = torch.empty(n * 32, dtype=torch.uint8, device=dev)
-    L = blk.lib()
+    from paper_2108_11560_b200 import build as _b
+    L = ctypes.CDLL(_b.build_diag())   # the split exists only in the diagnostics build
     f = L.blk_debug_split_f64
     f.restype = ctypes.c_int
     vp = ctypes.c_void_p
@@ -44,8 +45,7 @@ def main():
     split(1)()
     res = {}
     for name, fn in [("plan", split(1)), ("quad", split(2)), ("plan+quad", split(3)),
-                     ("fused simple", lambda: blk.bessel_logk_f64(vt, xt, *o, nbins=nb, kernel=1)),
-                     ("fused ws", lambda: blk.bessel_logk_f64(vt, xt, *o, nbins=nb, kernel=2))]:
+                     ("fused simple", lambda: blk.bessel_logk_f64(vt, xt, *o, nbins=nb, kernel=1))]:
         ms = timeit(fn)
         res[name] = ms
         print(f"{cfg} n={n} nbins={nb} {name:14s} {ms:.3f} ms  {n / ms * 1e3:.3e} evals/s", flush=True)

@@ -33,7 +33,8 @@ def main():
     xt = torch.from_numpy(x).to(dev).repeat(reps)[:nmax]
     o = [torch.empty_like(vt) for _ in range(3)]
     import ctypes
-    L = blk.lib()
+    from paper_2108_11560_b200 import build as _b
+    L = ctypes.CDLL(_b.build_diag())   # the split exists only in the diagnostics build
     f = L.blk_debug_split_f64
     f.restype = ctypes.c_int
     vp = ctypes.c_void_p
