@@ -1,23 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the fused sm_100a log K_v(x) + d/dv + d/dx kernel.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--nbins 128]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--nbins 128]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # the CPU oracle on host cores
 
 A step is one pass of the whole hot path (range finding + fixed-bin quadrature
-+ the three outputs) over one batch: config c2 of
-BASELINE.json (2^20 FP64 pairs, v~U[0,100], x~logU[0.1,1e3]) per GPU.  With
-N GPUs every rank processes its own 2^20-element batch (elements
-[r*2^20, (r+1)*2^20) of the same seeded stream): weak scaling, no collective
-on the data path; NCCL only reduces the timings (max over ranks).
++ the three outputs) over one batch.  The default workload
+is config c3 of BASELINE.json -- 2^24 FP64 pairs, v~logU[10,1000],
+x~logU[1e-3,10], all three outputs: the largest single-GPU FP64 config that
+asks for log K, d/dv and d/dx, which is what the metric names.  With N GPUs
+the one batch is split into N contiguous shards, one per rank (north_star
+(4)): strong scaling, no collective on the data path; NCCL only reduces the
+timings (max over ranks).  `--weak` gives every rank its own full batch.
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
 on the launching stream; between steps a 512 MiB buffer is written to flush
 L2 (outside the events).  Inputs are resident in HBM.  `e2e` repeats the
 metric through the C-ABI host-buffer entry point (pinned host arrays, which it
-reads and writes over PCIe from the kernel -- zero-copy; the 16 MiB of v, x and
-24 MiB of outputs cross PCIe inside the timed region).
+reads and writes over PCIe from the kernel -- zero-copy; v, x and the outputs
+cross PCIe inside the timed region).
+
+Roofline: the FP64 (or FP32) work per element of the kernel comes from an
+ncu capture of the current kernel sources (profiles/roofline_counts.json,
+written by tools/roofline_counts.py and stamped with the sha256 of the
+sources it was captured from); when the sources differ the line says
+"stale": true.  Peaks are measured in the same run (DFMA / FFMA / MUFU.EX2
+microbenchmarks: MEASURED_PEAKS.json has no FP64 figure).
 """
 from __future__ import annotations
 
@@ -37,20 +46,20 @@ import numpy as np  # noqa: E402
 
 import workloads  # noqa: E402
 
-# Per-element FP64 work of the fused kernel's algorithm (DFMA counted as 2
-# flops, DADD/DMUL as 1): the FP64 operations the kernel executes per element
-# (ncu sm__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on over one
-# launch / n) on config c2 at nbins=128 -- profiles/r01s2g_ncu_full_summary.txt,
-# DESIGN.md §5.  Used to turn the CUDA-event time into achieved FP64 FLOP/s.
-FP64_FLOPS_PER_ELEMENT = {("c2", 128): 4056.0}
-# FP32 entry point (c4, nbins=128), same method on the FP32 kernel
-# (profiles/r01_c4pk_ncu_full_summary.txt, SASS per-op counts): FP32 flops (FFMA=2,
-# FFMA2=4), the FP64 flops of its exponent formation and MUFU ops per element.
-FP32_WORK_PER_ELEMENT = {("c4", 128): {"fp32_flops": 2739.2, "fp64_flops": 1197.0, "mufu": 266.9}}
-# dram__bytes_read.sum + dram__bytes_write.sum of one launch (same capture),
-# per element; the outputs stay in L2 until after the kernel.
-DRAM_BYTES_PER_ELEMENT = {("c2", 128): 16.09}
-NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 (DESIGN.md §6)
+COUNTS = os.path.join(ROOT, "profiles", "roofline_counts.json")
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2 (DESIGN.md §5)
+
+
+def roofline_counts(cfg, nbins):
+    """(entry, stale, sha) for this workload from profiles/roofline_counts.json."""
+    from paper_2108_11560_b200.build import kernel_source_sha256
+    sha = kernel_source_sha256()
+    try:
+        data = json.load(open(COUNTS))
+    except (OSError, ValueError):
+        return None, True, sha
+    entry = data.get("captures", {}).get(f"{cfg}/{nbins}")
+    return entry, data.get("kernel_source_sha256") != sha, data.get("kernel_source_sha256")
 
 
 def parse():
@@ -59,15 +68,15 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2", choices=list(workloads.CONFIGS))
+    p.add_argument("--config", default="c3", choices=list(workloads.CONFIGS))
     p.add_argument("--nbins", type=int, default=128)
     p.add_argument("--n", type=int, default=0, help="override elements per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--out", default="")
-    p.add_argument("--strong", action="store_true",
-                   help="shard the config's batch over the ranks (default for c5)")
+    p.add_argument("--weak", action="store_true",
+                   help="every rank its own full batch (default: the one batch in N shards)")
     return p.parse_args()
 
 
@@ -103,7 +112,8 @@ def cpu_info():
 
 
 def oracle_rate(cfg, nbins, seconds, threads):
-    """Time the oracle (as it stands) on a bounded prefix sample of the workload."""
+    """Time the oracle (as it stands) on a bounded prefix sample of the workload.
+    Returns (evals/s, evaluations, seconds, sample elements)."""
     import oracle
     v, x = workloads.generate(cfg, 0, 2048)
     t = time.perf_counter()
@@ -123,7 +133,7 @@ def oracle_rate(cfg, nbins, seconds, threads):
         dt = time.perf_counter() - t
         if dt >= seconds * 0.9 or passes * n >= want:
             break
-    return passes * n / dt, passes * n, dt
+    return passes * n / dt, passes * n, dt, n
 
 
 class ClockSampler:
@@ -227,6 +237,14 @@ class ClockSampler:
                 "reasons": sorted(nm for nm, bit in self.REASONS if mask & bit)}
 
 
+def workload_config(args, c, total, world):
+    """The `config` object: the same keys and values for both arms."""
+    return {"workload": args.config, "describe": c.describe, "elements_total": total,
+            "nbins": args.nbins, "outputs": list(c.outputs),
+            "l2": "flushed between timed steps (512 MiB write, outside events)",
+            "parallelism": f"dp{world} (contiguous element shards, no collective)"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle on host cores (rank 0 only)."""
     if rank != 0:
@@ -235,24 +253,27 @@ def run_reference(args, rank, world):
     c = workloads.CONFIGS[args.config]
     per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     rates = []
-    n_used = 0
+    n_used = n_el = 0
     for i in range(args.warmup + args.steps):
-        r, n_used, _ = oracle_rate(args.config, args.nbins, per_step, cores)
+        r, n_used, _, n_el = oracle_rate(args.config, args.nbins, per_step, cores)
         if i >= args.warmup:
             rates.append(r)
     value = statistics.median(rates)
+    total = (args.n or c.n) * (args.gpus if args.weak else 1)
+    sample = (f"{n_used} evaluations per step: the first {n_el} elements of {args.config}, "
+              f"{n_used // max(1, n_el)} pass(es), {cores} threads, CPU {model}")
     line = {
-        "impl": "reference", "metric": "logK+dv+dx evals/sec FP64", "value": value,
+        "impl": "reference", "metric": "logK+dv+dx evals/sec FP64" if c.precision == "f64"
+        else "logK+dv+dx evals/sec FP32", "value": value,
         "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": n_used / value * 1e3, "higher_is_better": True,
-        "scaling": "strong" if (args.strong or args.config == "c5") else "weak",
+        "scaling": "weak" if args.weak else "strong",
         "vs_baseline": None, "dtype": "f64" if c.precision == "f64" else "f32",
-        "data": "synthetic (seeded, BASELINE.json config)",
-        "config": {"workload": args.config, "describe": c.describe, "nbins": args.nbins,
-                   "elements_per_step": n_used},
+        "data": "synthetic (seeded numpy PCG64 blocks, BASELINE.json config distribution)",
+        "config": workload_config(args, c, total, args.gpus),
+        "sample": sample,
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {n_used} elements of {args.config} per step, "
-                                   f"{cores} threads, CPU {model}"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -270,6 +291,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2108_11560_b200 as blk
+    from paper_2108_11560_b200.dist import shard_range
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -277,18 +299,17 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     c = workloads.CONFIGS[args.config]
     dt = torch.float64 if c.precision == "f64" else torch.float32
-    from paper_2108_11560_b200.dist import shard_range
-    if args.strong or args.config == "c5":
-        # strong scaling: the config's whole batch, contiguous shards (c5: 2^28 over N GPUs)
-        scaling = "strong"
-        total = args.n or c.n
-        lo, hi = shard_range(total, world, rank)
-    else:
+    if args.weak:
         # weak scaling: every rank its own batch of the config's size
         scaling = "weak"
         per = args.n or c.n
         total = per * world
         lo, hi = rank * per, (rank + 1) * per
+    else:
+        # strong scaling: the config's one batch in contiguous shards (north_star (4))
+        scaling = "strong"
+        total = args.n or c.n
+        lo, hi = shard_range(total, world, rank)
     n = hi - lo
     v_np, x_np = _generate_chunked(args.config, lo, n, total)
     v = torch.from_numpy(v_np).to(dev)
@@ -349,21 +370,21 @@ def main():
     total_ms = float(total_ms.item())
     ms_per_step = total_ms / args.steps
     value = total * args.steps / (total_ms * 1e-3)
+    local_ms = sum(step_ms) / args.steps        # this rank's kernel time per launch
 
-    # end to end through the host-buffer C-ABI entry point (FP64 configs)
+    # end to end through the host-buffer C-ABI entry point (pinned host
+    # buffers: zero-copy, no device workspace needed)
     e2e = None
     e2e_launches = 0
-    if not args.no_e2e and dt == torch.float64:
+    if not args.no_e2e:
         hv = torch.from_numpy(v_np).pin_memory()
         hx = torch.from_numpy(x_np).pin_memory()
         hout = {k: (torch.empty(n, dtype=dt).pin_memory() if k in c.outputs else None)
                 for k in ("logk", "dv", "dx")}
-        chunk = 1 << 18
-        ws = torch.empty(blk.host_workspace_bytes(chunk), dtype=torch.uint8, device=dev)
+        hfn = blk.bessel_logk_f64_host if dt == torch.float64 else blk.bessel_logk_f32_host
 
         def hstep():
-            blk.bessel_logk_f64_host(hv, hx, hout["logk"], hout["dv"], hout["dx"],
-                                     nbins=args.nbins, workspace=ws, chunk=chunk, stream=stream)
+            hfn(hv, hx, hout["logk"], hout["dv"], hout["dx"], nbins=args.nbins, stream=stream)
 
         for _ in range(2):
             hstep()
@@ -380,54 +401,59 @@ def main():
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         e2e_launches = args.steps   # zero-copy: one kernel launch per call
+        esz = 8 if dt == torch.float64 else 4
         e2e = {"value": total * args.steps / (float(e2e_ms.item()) * 1e-3), "unit": "evals/s",
-               "h2d_bytes_per_step": 2 * n * 8,
-               "d2h_bytes_per_step": len(c.outputs) * n * 8,
-               "path": "bessel_logk_f64_host (pinned host buffers: zero-copy, the kernel reads and writes them over PCIe)"}
+               "h2d_bytes_per_step": 2 * n * esz * world,
+               "d2h_bytes_per_step": len(c.outputs) * n * esz * world,
+               "path": f"{hfn.__name__} (pinned host buffers: zero-copy, the kernel reads and "
+                       "writes them over PCIe)"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    flops_pe = FP64_FLOPS_PER_ELEMENT.get((args.config, args.nbins))
+    counts, stale, counts_sha = roofline_counts(args.config, args.nbins)
+    rate = n / (local_ms * 1e-3)                # this rank's kernel, elements per second
+    esz = 8 if dt == torch.float64 else 4
+    alg_bytes = n * esz * (2 + len(c.outputs))
+    common = {"stale": stale, "counts": "profiles/roofline_counts.json" if counts else None,
+              "counts_source_sha256": counts_sha,
+              "kernel_time": "CUDA events around each launch on its stream (one launch per step)",
+              "algorithmic_bytes": alg_bytes,
+              "hbm_gbs": alg_bytes / (local_ms * 1e-3) / 1e9,
+              "traffic": counts["dram_bytes_per_element"] * n if counts else None,
+              "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)"}
     if dt == torch.float64:
-        peak_meas = fp64_ops * 2 / 1e12
-        if flops_pe:
-            ach = flops_pe * n / (ms_per_step * 1e-3) / 1e12
-        else:
-            ach = None
-        dbe = DRAM_BYTES_PER_ELEMENT.get((args.config, args.nbins))
-        roof = {"bound": "alu", "pipe": "fp64", "achieved": ach, "peak": peak_meas,
-                "unit": "TFLOP/s", "frac": (ach / peak_meas) if ach else None,
-                "traffic": (dbe * n) if dbe else None, "traffic_unit": "bytes per launch (ncu)",
-                "algorithmic_bytes": n * (16 + 8 * len(c.outputs)),
-                "peak_source": "in-run DFMA microbenchmark (blk_microbench_fp64); nominal "
-                               f"{NOMINAL_FP64_TFLOPS:.1f} TF/s from 148 SM x 64 DFMA/clk x 1.965 GHz",
-                "flops_per_element": flops_pe,
-                "hbm_gbs": (n * (16 + 8 * len(c.outputs))) / (ms_per_step * 1e-3) / 1e9}
+        peak = fp64_ops * 2 / 1e12
+        ach = counts["fp64_flops_per_element"] * rate / 1e12 if counts else None
+        iss = counts["fp64_inst_per_element"] * rate if counts else None
+        roof = {"bound": "alu", "pipe": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak if ach else None,
+                "fp64_issue": {"achieved_inst_per_s": iss, "peak_inst_per_s": fp64_ops,
+                               "frac": iss / fp64_ops if iss else None,
+                               "inst_per_element": counts["fp64_inst_per_element"] if counts else None},
+                "flops_per_element": counts["fp64_flops_per_element"] if counts else None,
+                "peak_source": "in-run DFMA microbenchmark (blk_microbench_fp64; 2 flops per DFMA); "
+                               f"nominal {NOMINAL_FP64_TFLOPS:.1f} TF/s = 148 SM x 64 DFMA/clk x 1.965 GHz"}
     else:
-        wk = FP32_WORK_PER_ELEMENT.get((args.config, args.nbins))
-        rate = n / (ms_per_step * 1e-3)
-        ach = wk["fp32_flops"] * rate / 1e12 if wk else None
         peak32 = fp32_ops * 2 / 1e12
-        roof = {"bound": "alu", "pipe": "fp32 (with fp64 exponent and MUFU)", "achieved": ach,
-                "peak": peak32, "unit": "TFLOP/s", "frac": (ach / peak32) if ach else None,
-                "traffic": None,
-                "fp64_tflops": wk["fp64_flops"] * rate / 1e12 if wk else None,
-                "fp64_frac": (wk["fp64_flops"] * rate / 1e12) / (fp64_ops * 2 / 1e12) if wk else None,
-                "mufu_frac": (wk["mufu"] * rate) / mufu_ops if wk else None,
-                "peak_source": "in-run FFMA/DFMA/MUFU.EX2 microbenchmarks; the kernel is bound by "
-                               "register-file reads across the three pipes (DESIGN.md §5)",
-                "hbm_gbs": (n * 20) / (ms_per_step * 1e-3) / 1e9}
+        ach = counts["fp32_flops_per_element"] * rate / 1e12 if counts else None
+        roof = {"bound": "alu", "pipe": "fp32 (+ fp64 exponent, MUFU)", "achieved": ach,
+                "peak": peak32, "unit": "TFLOP/s", "frac": ach / peak32 if ach else None,
+                "fp64_frac": (counts["fp64_flops_per_element"] * rate / 1e12) / (fp64_ops * 2 / 1e12)
+                if counts else None,
+                "mufu_frac": counts["mufu_per_element"] * rate / mufu_ops if counts else None,
+                "peak_source": "in-run FFMA/DFMA/MUFU.EX2 microbenchmarks"}
+    roof.update(common)
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cores, model = cpu_info()
-        r, ns, secs = oracle_rate(args.config, args.nbins, args.cpu_seconds, cores)
+        r, ns, secs, nel = oracle_rate(args.config, args.nbins, args.cpu_seconds, cores)
         cpu = {"value": r, "unit": "evals/s", "cores": cores, "kind": "oracle",
-               "sample": f"{ns} evaluations over the first {min(ns, workloads.CONFIGS[args.config].n, 1 << 22)} "
-                          f"elements of {args.config} ({secs:.1f} s, {cores} threads, {model})"}
+               "sample": f"{ns} evaluations: the first {nel} elements of {args.config}, "
+                         f"{ns // max(1, nel)} pass(es) ({secs:.1f} s, {cores} threads, {model})"}
 
     line = {
         "metric": "logK+dv+dx evals/sec FP64" if dt == torch.float64 else "logK+dv+dx evals/sec FP32",
@@ -435,11 +461,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64" if dt == torch.float64 else "f32",
         "data": "synthetic (seeded numpy PCG64 blocks, BASELINE.json config distribution)",
-        "config": {"workload": args.config, "describe": c.describe, "elements_total": total,
-                   "elements_per_gpu": n,
-                   "nbins": args.nbins, "outputs": list(c.outputs),
-                   "l2": "flushed between timed steps (512 MiB write, outside events)",
-                   "parallelism": f"dp{world} (contiguous element shards, no collective)"},
+        "config": workload_config(args, c, total, world),
+        "elements_per_gpu": n,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

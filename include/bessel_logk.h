@@ -161,6 +161,25 @@ BLK_API blk_status bessel_logk_f32_host(const float *v, const float *x, size_t n
                                 size_t chunk, cudaStream_t stream);
 
 /*
+ * The integration plan alone: Alg. 3 lines 2-9 (Alg. 1 FindRange,
+ * Alg. 2 FindZero) exactly as bessel_logk_f64 / _f64_ex find it
+ * for the same nbins and options (range_mode selects the finder as there;
+ * lanes_per_element does not change the plan):
+ *   tp[i] = t_p (0 when v^2 <= x), gp[i] = g(t_p) (the log-sum-exp
+ *   shift of Eq. (int)), t0[i], t1[i] = the ends of the range where
+ *   g >= g(t_p) + log eps, eps = 2^-52.
+ * bessel_logk_f64 integrates Eq. (int) with n = nbins intervals over exactly
+ * [t0[i], t1[i]] with shift gp[i].  All pointers DEVICE, n doubles each; any
+ * output may be NULL (at least one not).  NaN where the element has no plan
+ * (invalid input, FindRange cap).  Several plans are equally correct (any
+ * conservative range, R20); this one lets a caller check the
+ * quadrature against a reference on the same range.
+ */
+BLK_API blk_status bessel_logk_plan_f64(const double *v, const double *x, size_t n, double *tp,
+                                        double *gp, double *t0, double *t1, int nbins,
+                                        const blk_options *opts, cudaStream_t stream);
+
+/*
  * Second derivatives in the same pass: from the
  * second-order differentiated integrands of Sec. 4.1 (f^{(n,m)},
  * n+m = 2) over f's range and nodes,

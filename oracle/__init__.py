@@ -70,6 +70,9 @@ def _load():
             lib.oracle_logk_own_range.restype = ctypes.c_int
             lib.oracle_logk_own_range.argtypes = [dp, dp, ctypes.c_size_t, dp, dp, dp,
                                                   ctypes.c_int, ctypes.c_double]
+            lib.oracle_quad_on_plan.restype = ctypes.c_int
+            lib.oracle_quad_on_plan.argtypes = [dp, dp, ctypes.c_size_t, dp, dp, dp, dp, dp, dp,
+                                                ctypes.c_int]
             lib.oracle_log_eps_f64.restype = ctypes.c_double
             lib.oracle_log_eps_f32.restype = ctypes.c_double
             _lib = lib
@@ -132,6 +135,32 @@ def logk(v, x, nbins: int = 128, *, max_iter: int = MAX_ITER, tol: float = 0.0,
                         range(threads)))
     if with_plan:
         return out[0], out[1], out[2], plan
+    return out[0], out[1], out[2]
+
+
+def quad_on_plan(v, x, gp, t0, t1, nbins: int = 128, threads: int = 1):
+    """Eq. (int) on a given plan (g(t_p), t0, t1 per element): log K, dlogK/dv,
+    dlogK/dx.  Used to check another implementation's quadrature on ITS range
+    (several plans are correct, R20; the outputs on a given plan are unique)."""
+    lib = _load()
+    arrs = [_as_f64(a).ravel() for a in (v, x, gp, t0, t1)]
+    n = arrs[0].size
+    out = [np.empty(n), np.empty(n), np.empty(n)]
+
+    def run(lo, hi):
+        if hi > lo:
+            p = [a.ctypes.data + 8 * lo for a in arrs]
+            rc = lib.oracle_quad_on_plan(p[0], p[1], hi - lo, p[2], p[3], p[4],
+                                         *[o.ctypes.data + 8 * lo for o in out], int(nbins))
+            if rc != 0:
+                raise ValueError("oracle_quad_on_plan: invalid arguments")
+
+    if threads <= 1 or n < 1024:
+        run(0, n)
+    else:
+        bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda k: run(int(bounds[k]), int(bounds[k + 1])), range(threads)))
     return out[0], out[1], out[2]
 
 

@@ -166,6 +166,42 @@ static int oracle_plan(oracle_ctx *c, int max_iter, double tol,
 }
 
 /*
+ * Eq. (int) on the range [t0, t1] with shift c->gp = g(t_p):
+ * n = nbins trapezoid intervals, nodes t_m = t0 + m h, h = (t1 - t0)/n,
+ * weights c_0 = c_n = 1/2, else 1, multiplying the exponential (R7):
+ *   S0 = sum c_m e^{g(t_m) - g_p},  log K = g_p + log h + log S0
+ * and the derivative integrands of Sec. 4.1 on the same nodes (R14):
+ *   S1 = sum c_m e^{g - g_p} t tanh(vt)  -> dlogK/dv = sign(v) S1/S0
+ *   S2 = sum c_m e^{g - g_p} cosh t      -> dlogK/dx = -S2/S0
+ * (+ the second-order sums when hess != NULL, see oracle_one_h).
+ */
+static void oracle_quadrature(const oracle_ctx *c, double s, double t0, double t1, int nbins,
+                              double *logk, double *dv, double *dx, double *hess)
+{
+    double h = (t1 - t0) / nbins;
+    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0;
+    for (int m = 0; m <= nbins; ++m) {
+        double t = t0 + m * h;
+        double cm = (m == 0 || m == nbins) ? 0.5 : 1.0;
+        double w = cm * exp(g0(c, t) - c->gp);
+        S0 += w;
+        S1 += w * t * tanh(c->v * t);
+        S2 += w * cosh(t);
+        S11 += w * t * t;
+        S22 += w * cosh(t) * cosh(t);
+        S12 += w * t * tanh(c->v * t) * cosh(t);
+    }
+    *logk = c->gp + log(h) + log(S0);
+    *dv = s * S1 / S0;
+    *dx = -S2 / S0;
+    if (hess) {
+        hess[0] = S11 / S0 - (S1 / S0) * (S1 / S0);
+        hess[1] = S22 / S0 - (S2 / S0) * (S2 / S0);
+        hess[2] = s * (-S12 / S0 + (S1 / S0) * (S2 / S0));
+    }
+}
+
+/*
  * One element.  Eq. (int) with the weights c_m multiplying the
  * exponential (R7), the derivative integrands of Sec. 4.1
  * d/dv f = t sinh(vt) e^{-x cosh t} = f t tanh(vt),  d/dx f = -cosh t f,
@@ -213,27 +249,7 @@ static void oracle_one_h(double v_in, double x, int nbins, int max_iter, double 
         return;
     }
     if (plan) { plan[0] = tp; plan[1] = c.gp; plan[2] = t0; plan[3] = t1; }
-    double h = (t1 - t0) / nbins;                        /* P:228 */
-    double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0;
-    for (int m = 0; m <= nbins; ++m) {
-        double t = t0 + m * h;                           /* P:228 */
-        double cm = (m == 0 || m == nbins) ? 0.5 : 1.0;  /* P:231 */
-        double w = cm * exp(g0(&c, t) - c.gp);
-        S0 += w;
-        S1 += w * t * tanh(c.v * t);
-        S2 += w * cosh(t);
-        S11 += w * t * t;
-        S22 += w * cosh(t) * cosh(t);
-        S12 += w * t * tanh(c.v * t) * cosh(t);
-    }
-    *logk = c.gp + log(h) + log(S0);                     /* P:236 */
-    *dv = s * S1 / S0;
-    *dx = -S2 / S0;
-    if (hess) {
-        hess[0] = S11 / S0 - (S1 / S0) * (S1 / S0);
-        hess[1] = S22 / S0 - (S2 / S0) * (S2 / S0);
-        hess[2] = s * (-S12 / S0 + (S1 / S0) * (S2 / S0));
-    }
+    oracle_quadrature(&c, s, t0, t1, nbins, logk, dv, dx, hess);
 }
 
 /*
@@ -325,6 +341,32 @@ int oracle_logk(const double *v, const double *x, size_t n,
         double a, b, d;
         oracle_one(v[i], x[i], nbins, max_iter, tol, log_eps, &a, &b, &d,
                    plan ? plan + 4 * i : NULL);
+        if (logk) logk[i] = a;
+        if (dlogk_dv) dlogk_dv[i] = b;
+        if (dlogk_dx) dlogk_dx[i] = d;
+    }
+    return 0;
+}
+
+/*
+ * Eq. (int) on a GIVEN plan (gp, t0, t1 per element; host arrays of n
+ * doubles), for checking a quadrature on another implementation's range
+ * (several plans are correct, R20): the outputs are then unique.  NaN plan
+ * entries or invalid inputs give NaN outputs.
+ */
+int oracle_quad_on_plan(const double *v, const double *x, size_t n, const double *gp,
+                        const double *t0, const double *t1, double *logk, double *dlogk_dv,
+                        double *dlogk_dx, int nbins)
+{
+    if (nbins < 1)
+        return -1;
+    for (size_t i = 0; i < n; ++i) {
+        double a = NAN, b = NAN, d = NAN;
+        if (x[i] > 0.0 && isfinite(x[i]) && isfinite(v[i]) && isfinite(gp[i]) &&
+            isfinite(t0[i]) && isfinite(t1[i])) {
+            oracle_ctx c = { fabs(v[i]), x[i], gp[i], 0.0 };
+            oracle_quadrature(&c, (v[i] < 0.0) ? -1.0 : 1.0, t0[i], t1[i], nbins, &a, &b, &d, NULL);
+        }
         if (logk) logk[i] = a;
         if (dlogk_dv) dlogk_dv[i] = b;
         if (dlogk_dx) dlogk_dx[i] = d;

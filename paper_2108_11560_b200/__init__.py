@@ -25,6 +25,7 @@ __all__ = [
     "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
     "bessel_logk_f32_host",
     "host_workspace_bytes", "microbench", "DEFAULT_NBINS", "nig_loglik", "log_bessel_k_hess",
+    "bessel_logk_plan_f64",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -83,6 +84,9 @@ def lib():
         L.bessel_logk_version.restype = ctypes.c_char_p
         L.bessel_logk_hess_f64.restype = ci
         L.bessel_logk_hess_f64.argtypes = [vp, vp, sz, vp, vp, vp, vp, vp, vp, ci,
+                                           ctypes.POINTER(_Options), vp]
+        L.bessel_logk_plan_f64.restype = ci
+        L.bessel_logk_plan_f64.argtypes = [vp, vp, sz, vp, vp, vp, vp, ci,
                                            ctypes.POINTER(_Options), vp]
         L.bessel_nig_workspace_bytes.restype = sz
         L.bessel_nig_workspace_bytes.argtypes = [sz]
@@ -322,6 +326,28 @@ def log_bessel_k_hess(v, x, nbins=DEFAULT_NBINS, stream=None, lanes_per_element=
     o = _Options(int(lanes_per_element), int(range_mode), 0, 0)
     with torch.cuda.device(dev):
         _check(lib().bessel_logk_hess_f64(pv, px, n, *[ctypes.c_void_p(t.data_ptr()) for t in outs],
+                                          int(nbins), ctypes.byref(o),
+                                          ctypes.c_void_p(st.cuda_stream)))
+    _keep_alive(st, *outs)
+    return tuple(outs)
+
+
+def bessel_logk_plan_f64(v, x, nbins=DEFAULT_NBINS, stream=None, range_mode=BLK_RANGE_AUTO):
+    """The integration plan (t_p, g(t_p), t0, t1) the FP64 entry point integrates
+    over for this nbins and range_mode, as four float64 CUDA tensors (NaN where an
+    element has none).  See include/bessel_logk.h (bessel_logk_plan_f64)."""
+    import torch
+    if not isinstance(v, torch.Tensor) or not v.is_cuda:
+        raise TypeError("v must be a CUDA tensor")
+    dev = v.device
+    n = v.numel()
+    pv = _dev_ptr(v, torch.float64, n, "v", dev)
+    px = _dev_ptr(x, torch.float64, n, "x", dev)
+    st = _stream_for(stream, dev)
+    outs = [torch.empty_like(v) for _ in range(4)]
+    o = _Options(0, int(range_mode), 0, 0)
+    with torch.cuda.device(dev):
+        _check(lib().bessel_logk_plan_f64(pv, px, n, *[ctypes.c_void_p(t.data_ptr()) for t in outs],
                                           int(nbins), ctypes.byref(o),
                                           ctypes.c_void_p(st.cuda_stream)))
     _keep_alive(st, *outs)

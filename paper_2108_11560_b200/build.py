@@ -40,6 +40,21 @@ def _deps():
             + [os.path.join(ROOT, "include", "bessel_logk.h")])
 
 
+def kernel_source_sha256() -> str:
+    """sha256 of everything that determines the kernels' instruction stream
+    (csrc sources, the header, the build flags in this file): bench.py marks a
+    roofline whose ncu counts were captured from other sources as stale."""
+    import hashlib
+    files = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                   + glob.glob(os.path.join(CSRC, "*.inc")))
+    files += [os.path.join(ROOT, "include", "bessel_logk.h"), os.path.abspath(__file__)]
+    h = hashlib.sha256()
+    for f in files:
+        h.update(os.path.relpath(f, ROOT).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()
+
+
 def is_stale() -> bool:
     if not os.path.exists(LIB):
         return True

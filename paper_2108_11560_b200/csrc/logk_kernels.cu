@@ -70,6 +70,28 @@ __device__ __forceinline__ void lane_bins(int n, int sub, int &mb, int &me) {
   me = min(mb + per, n + 1);
 }
 
+// a2-a5 for one canonical element (v >= 0, x > 0 finite) of the FP64 entry
+// point: the range finder BLK_RANGE_AUTO / BLK_RANGE_F64 selects (FP32 from
+// 64 bins inside its domain, else FP64 with the table exp, which needs
+// g_exp_tab loaded), t_p, g(t_p), [t0, t1] and dmin.  Returns whether the plan
+// is usable.  Shared by the fused kernels and the plan export, so
+// bessel_logk_plan_f64 reports exactly the plan the quadrature uses.
+template <int LPE>
+__device__ __forceinline__ bool element_plan_f64(double v, double x, int nbins, int range_mode,
+                                                 int sub, double &tp, double &gp, double &t0,
+                                                 double &t1, double &dmin) {
+  bool ok;
+  if (use_f32_plan(range_mode, nbins, v, x)) {
+    const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
+                                     : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
+    ok = p.ok; tp = p.tp; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
+  } else {
+    const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
+    ok = p.ok; tp = p.tp; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
+  }
+  return ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+}
+
 template <bool LOGK, bool DV, bool DX, int LPE>
 __global__ void __launch_bounds__(128, BLK_MINB)
 logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
@@ -94,19 +116,8 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
 
   // a2-a5: integration plan (t_p, g(t_p), t0, t1)
-  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
-  bool ok = false;
-  if (valid) {
-    if (use_f32_plan(range_mode, nbins, v, x)) {
-      const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
-                                       : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
-      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
-    } else {
-      const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
-      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
-    }
-    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
-  }
+  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;
+  const bool ok = valid && element_plan_f64<LPE>(v, x, nbins, range_mode, sub, tp, gp, t0, t1, dmin);
   BLK_TL(1);
   // a6: fixed-bin quadrature, three sums in one pass
   Sums64 s{0.0, 0.0, 0.0};
@@ -155,19 +166,8 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
   const double v = fabs(vraw);
   const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
-  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0;
-  bool ok = false;
-  if (valid) {
-    if (use_f32_plan(range_mode, nbins, v, x)) {
-      const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
-                                       : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
-      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
-    } else {
-      const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
-      ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
-    }
-    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
-  }
+  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;
+  const bool ok = valid && element_plan_f64<LPE>(v, x, nbins, range_mode, sub, tp, gp, t0, t1, dmin);
   Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double h = (t1 - t0) * rcp64((double)nbins);
   if (ok) {
@@ -190,6 +190,29 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   if (dvv_out) dvv_out[i] = ok ? fma(-m1, m1, s.S11 * r) : nanv;
   if (dxx_out) dxx_out[i] = ok ? fma(-m2, m2, s.S22 * r) : nanv;
   if (dvx_out) dvx_out[i] = ok ? sgn * fma(m1, m2, -(s.S12 * r)) : nanv;
+}
+
+// The plan alone (bessel_logk_plan_f64): what the FP64 entry point integrates
+// over for the same nbins and range_mode; NaN where it has no usable plan.
+__global__ void __launch_bounds__(128)
+logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
+                     double *__restrict__ tp_out, double *__restrict__ gp_out,
+                     double *__restrict__ t0_out, double *__restrict__ t1_out, int nbins,
+                     int range_mode) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double vraw = i < n_el ? vin[i] : 1.0;
+  const double x = i < n_el ? xin[i] : 1.0;
+  load_exp_table();
+  __syncthreads();
+  if (i >= n_el) return;
+  const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
+  double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;
+  const bool ok = valid && element_plan_f64<1>(fabs(vraw), x, nbins, range_mode, 0, tp, gp, t0, t1, dmin);
+  const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
+  if (tp_out) tp_out[i] = ok ? tp : nanv;
+  if (gp_out) gp_out[i] = ok ? gp : nanv;
+  if (t0_out) t0_out[i] = ok ? t0 : nanv;
+  if (t1_out) t1_out[i] = ok ? t1 : nanv;
 }
 
 #ifndef BLK_F32_MINB
@@ -629,6 +652,23 @@ blk_status bessel_nig_loglik_f64(const double *y, size_t n, double alpha, double
   blk::nig_final_kernel<<<1, 256, 0, s>>>(partial, blocks, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BLK_OK : cuda_fail(e, "nig kernels");
+}
+
+blk_status bessel_logk_plan_f64(const double *v, const double *x, size_t n, double *tp,
+                                double *gp, double *t0, double *t1, int nbins,
+                                const blk_options *opts, cudaStream_t stream) {
+  int lanes, mode, th, kernel;
+  const bool any = tp || gp || t0 || t1;
+  blk_status st = validate(v, x, n, any ? (void *)1 : nullptr, nullptr, nullptr, nbins, opts,
+                           lanes, mode, th, kernel);
+  if (st != BLK_OK) return st;
+  if (n == 0) return BLK_OK;
+  const size_t blocks = (n + 127) / 128;
+  if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "grid too large");
+  blk::logk_plan_f64_kernel<<<(unsigned)blocks, 128, 0, stream>>>(v, x, n, tp, gp, t0, t1, nbins,
+                                                                  mode);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BLK_OK : cuda_fail(e, "plan kernel launch");
 }
 
 blk_status bessel_logk_hess_f64(const double *v, const double *x, size_t n, double *logk,

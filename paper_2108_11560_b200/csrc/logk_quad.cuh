@@ -577,6 +577,26 @@ __device__ __forceinline__ void end_half_f32(double v, double x, double s_mid, d
   }
 }
 
+// The same in FP64 (exact state, libm-accurate cosh, clamped exponent): for
+// coarse grids (n < kEndF32MinBins), whose sums can miss the peak by far more
+// than the node's own eps level -- at 2 bins over a range 30 wide the sums
+// are of the same order as node n's term.
+template <bool DV, bool DX, bool HESS>
+__device__ __forceinline__ void end_half_f64(double v, double x, double s_mid, double t,
+                                             Sums64 &s) {
+  const double et = exp_cw(fmin(t, 709.0));
+  const double ch = 0.5 * (et + rcp64(et));
+  const double z2 = fmax(-2.0 * v * t, -707.0);
+  Sums64 z{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  node_acc<DV, DX, HESS, true>(v, x, s_mid, t, ch, exp_cw(z2), one_minus_exp(z2), z);
+  s.S0 -= 0.5 * z.S0; s.S1 -= 0.5 * z.S1; s.S2 -= 0.5 * z.S2;
+  s.S11 -= 0.5 * z.S11; s.S22 -= 0.5 * z.S22; s.S12 -= 0.5 * z.S12;
+}
+// From this many bins the node nearest the peak is within 36/n^2 < 0.01 (log
+// units) of it, so S0 is at least ~the peak term and node n's (< eps of the
+// peak) is resolved by FP32.
+constexpr int kEndF32MinBins = 64;
+
 // Nodes [mb, me) of the n-interval trapezoid on [t0, t0 + n h] (node m at
 // t0 + m h; nodes 0 and n carry weight 1/2: all nodes are summed
 // with weight 1 and half of each end node is taken back).  The lane owning
@@ -597,7 +617,10 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
     nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, s);
   // node n: t_n = t1 lies outside the eps-support (d(t1) < 0, FindZero
   // returns the outer end, R1), so its term is < 2^-52 of the peak term
-  if (mb < me && me == n + 1) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
+  if (mb < me && me == n + 1) {
+    if (n >= kEndF32MinBins) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
+    else end_half_f64<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
+  }
   return s;
 }
 

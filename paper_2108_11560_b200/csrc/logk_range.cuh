@@ -177,10 +177,11 @@ __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
 // but how far g(a) lies below the maximum, because g(t_p) becomes the
 // log-sum-exp shift and the base of the eps threshold: Newton's estimate of
 // that gap is F(a)^2 / (2 |F'(a)|), and the search stops once it is below
-// kPeakGapTol (1/16 in log units).  A relative criterion on t_p would leave
-// gaps of |g''| (tol t_p)^2 / 2 -- over 100 in log units for x ~ 1e-30 and
-// v ~ 1e4 (t_p ~ 78), enough to push FP32 weights out of range.
-constexpr float kPeakGapTol = 0.0625f;
+// 16 tol in log units (1/16 at the 2^-8 tier of 128+ bins, 1/64 at 64-127).
+// A relative criterion on t_p would leave gaps of |g''| (tol t_p)^2 / 2 --
+// over 100 in log units for x ~ 1e-30 and v ~ 1e4 (t_p ~ 78), enough to push
+// FP32 weights out of range, and 0.6 at 64 bins for v ~ 2500, x ~ 1e-6.
+constexpr float kPeakGapPerTol = 16.0f;
 // For the range ends the Newton correction is measured against the distance
 // of a from the peak t_p (`ref`), the scale of the half-range, not against
 // |a|: for a far peak (t_p ~ 14 with a half-range of 0.3) |a| would allow
@@ -192,9 +193,8 @@ __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, fl
   for (int i = 0; i < kMaxIter; ++i) {
     // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
     // carries no information and must not end the search)
-    if (PEAK && tol >= 3e-3f) {
-      // (at 64-127 bins, tol = 2^-10, the peak is found like the range ends)
-      if (Fa * Fa <= (2.0f * kPeakGapTol) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
+    if (PEAK) {
+      if (Fa * Fa <= (2.0f * kPeakGapPerTol * tol) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
     } else {
       const float rhs = tol * fabsf((a - ref) * dFa);
       if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;

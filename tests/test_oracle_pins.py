@@ -424,94 +424,7 @@ def test_cancellation_band_vs_brute_force():
 
 
 # ------------------------------------------------- the plan vs mpmath roots
-_L_MP = None
-
-
-def _mp_root(f, a, b):
-    """Bisection to ~1e-26 relative on a sign change of f over (a, b)."""
-    fa = f(a)
-    assert fa * f(b) < 0
-    tol = mpmath.mpf(10) ** -26
-    while b - a > tol * max(1, abs(a)):
-        m = (a + b) / 2
-        fm = f(m)
-        if fm == 0:
-            return m
-        if (fm > 0) == (fa > 0):
-            a, fa = m, fm
-        else:
-            b = m
-    return (a + b) / 2
-
-
-def _mp_doubling(F, ts):
-    """Alg. 1's bracket width from t_s (reading R5), with the exact
-    F: m = min{m >= 0 : F(t_s + 2^(m+1)) < 0}; width 2 when m = 0, else 2^m."""
-    m = 0
-    while F(ts + mpmath.mpf(2) ** (m + 1)) >= 0:
-        m += 1
-    return 2.0 if m == 0 else float(2 ** m)
-
-
-def mp_plan(v, x):
-    """The exact plan at 30 digits, from the definitions only (P:91-96,
-    P:121-133): t_p* the root of g' = v tanh(vt) - x sinh t (0 when
-    v^2 <= x), t0*, t1* the roots of d(t) = g(t) - g(t_p*) - log eps left and
-    right of it (t0* = 0 when d(0) <= 0 has no root), plus Alg. 1's initial
-    bracket widths W0 of the three searches (2^m, the t0 search: t_p)."""
-    with mpmath.workdps(30):
-        v, x = mpmath.mpf(float(v)), mpmath.mpf(float(x))
-        L = mpmath.log(mpmath.mpf(2) ** -52)
-
-        def g(t):
-            return mpmath.log(mpmath.cosh(v * t)) - x * mpmath.cosh(t)
-
-        def g1(t):
-            return v * mpmath.tanh(v * t) - x * mpmath.sinh(t)
-
-        tp, w_tp = mpmath.mpf(0), 0.0
-        if v * v - x > 0:
-            w_tp = _mp_doubling(g1, mpmath.mpf(0))
-            hi = mpmath.mpf(2)
-            while g1(hi) > 0:
-                hi *= 2
-            tp = _mp_root(g1, hi * mpmath.mpf(10) ** -30, hi)
-        gp = g(tp)
-
-        def d(t):
-            return g(t) - gp - L
-
-        t0 = mpmath.mpf(0)
-        d0 = float(d(mpmath.mpf(0)))
-        if d0 <= 0:
-            t0 = _mp_root(d, mpmath.mpf(0), tp)
-        w_t1 = _mp_doubling(d, tp)
-        hi = tp + 2
-        while d(hi) >= 0:
-            hi = tp + 2 * (hi - tp)
-        t1 = _mp_root(d, tp, hi)
-        return (float(tp), float(t0), float(t1)), (w_tp, float(tp), w_t1), d0
-
-
-def plan_violations(v, x, plan, exact):
-    """Per element, whether the oracle's (t_p, t0, t1) break the pin:
-      * orientation (R1, Alg. 2 keeps F(a) < 0 and returns a): t_p >= t_p*,
-        t0 <= t0*, t1 >= t1* -- the range is conservative;
-      * the 10-iteration bound: every iteration of Alg. 2 at least halves the
-        bracket (t_shrink, and the Newton point clipped to [a, t_shrink]), so
-        |t - t*| <= W0 2^-10 with W0 Alg. 1's bracket (t_p for the t0 search).
-    Slack 1e-12 max(1, t*) for double rounding of F near its zero."""
-    bad = []
-    for i in range(len(v)):
-        (tp_s, t0_s, t1_s), (w_tp, w_t0, w_t1), _ = exact[i]
-        tp, _, t0, t1 = plan[i]
-        out = False
-        for t, ts, w, side in ((tp, tp_s, w_tp, +1), (t0, t0_s, w_t0, -1), (t1, t1_s, w_t1, +1)):
-            slack = 1e-12 * max(1.0, abs(ts))
-            if side * (t - ts) < -slack or abs(t - ts) > w * 2.0 ** -10 + slack:
-                out = True
-        bad.append(out)
-    return np.array(bad)
+from plan_pins import mp_plan, plan_violations  # noqa: E402
 
 
 @pytest.fixture(scope="module")
