@@ -105,14 +105,18 @@ def plan_check_f32(v, x, plan, exact, tol):
         bracket) plus e_d;
       * each range end lies on the outer side of the root of its OWN
         threshold g(t) = g_p + log eps (so also of the exact eps-support,
-        g_p <= g(t_p*)), within 2 tol |t - t_p*| + e_d / |g'| of it;
+        g_p <= g(t_p*)), within max(2 tol |t - t_p*|, W0 2^-10) + e_d / |g'|
+        of it (the stopping rule, or the 10-iteration bracket when Alg. 2's
+        preference for the bisection point keeps Newton from converging --
+        e.g. t1 for large x: bisection steps 2 -> 1 -> ... -> 0.0317 against
+        the root 0.03125 after 10 iterations);
     e_d = 2^-20 (|g_p| + x cosh t + v t + 40) is the FP32 resolution of d.
     Returns the per-element violation mask."""
     bad = []
     with mpmath.workdps(30):
         L = mpmath.log(mpmath.mpf(2) ** -52)
         for i in range(len(v)):
-            (tp_s, t0_s, t1_s), (w_tp, _, _), _ = exact[i]
+            (tp_s, t0_s, t1_s), (w_tp, w_t0, w_t1), _ = exact[i]
             _, gp, t0, t1 = plan[i]
             vv, xx = mpmath.mpf(float(v[i])), mpmath.mpf(float(x[i]))
 
@@ -134,7 +138,7 @@ def plan_check_f32(v, x, plan, exact, tol):
             def d(t):
                 return g(t) - mpmath.mpf(gp) - L
 
-            for t, side in ((t0, -1), (t1, +1)):
+            for t, side, w0 in ((t0, -1, w_t0), (t1, +1, w_t1)):
                 if side < 0 and d(mpmath.mpf(0)) > 0:
                     out |= t != 0.0
                     continue
@@ -149,7 +153,8 @@ def plan_check_f32(v, x, plan, exact, tol):
                 ed = 2.0 ** -20 * (abs(gp) + float(x[i]) * float(mpmath.cosh(ts)) + float(v[i]) * float(ts) + 40.0)
                 res = ed / max(slope, 1e-300)
                 tsf = float(ts)
-                if side * (t - tsf) < -res or abs(t - tsf) > 2 * tol * abs(tsf - tp_s) + res:
+                if side * (t - tsf) < -res or abs(t - tsf) > max(2 * tol * abs(tsf - tp_s),
+                                                                w0 * 2.0 ** -10) + res:
                     out = True
             bad.append(out)
     return np.array(bad)
