@@ -216,9 +216,9 @@ logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ 
 }
 
 #ifndef BLK_F32_MINB
-// FP32 entry point: 6 resident blocks per SM (ptxas then fits 80 registers;
-// unconstrained it took 96 and ran 5): c4 +3.2% (profiles/r01s3h_f32_minb.log)
-#define BLK_F32_MINB 6
+// FP32 entry point: 5 resident blocks per SM (96 registers; the v3 loop
+// spills at 6 blocks / 80 registers: c4 -4%, profiles/r02e_f32v3.log)
+#define BLK_F32_MINB 5
 #endif
 template <bool LOGK, bool DV, bool DX, int LPE>
 __global__ void __launch_bounds__(128, BLK_F32_MINB)
@@ -240,8 +240,8 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   if (valid) {
     if (use_f32_plan(range_mode, nbins, v, x)) {
       const Plan<float> p =
-          (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF32, fz_tol_for(nbins), sub & 1)
-                     : make_plan_f32(v, x, kLogEpsF32, fz_tol_for(nbins));
+          (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF32, fz_tol_f32_entry(nbins), sub & 1)
+                     : make_plan_f32(v, x, kLogEpsF32, fz_tol_f32_entry(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);
@@ -257,8 +257,11 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
     // the fixed-point exponent needs every node within 2^-126 of the peak:
     // true when both range ends are < 60 below the log-eps level (always on
     // ranges found by Alg. 1-3; kept exact for safety)
-#ifndef BLK_F32_V1
+#if defined(BLK_F32_V2)
     if (dmin > -60.0f) s = quad_f32_v2<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
+    else
+#elif !defined(BLK_F32_V1)
+    if (dmin > -60.0f) s = quad_f32_v3<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
     else
 #endif
       s = quad_f32<DV, DX>(v, x, t0, h, gp, nbins, mb, me);

@@ -892,4 +892,136 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
   return Sums32{S0, S1, S2};
 }
 
+// FP32 entry point, group-base form (v3).  The FP64 fixed-point exponent of
+// quad_f32_v2 is formed once per group of 4 nodes, at the group's first node
+// c: A_c = v2 t_c - X_c + cst (X = x cosh t log2(e) = Xp + Xm, Xp/m =
+// (x log2(e)/2) e^{+-t}; 7 FP64 operations), E_c = 2^{a2_c} by exp2_fixed.
+// The other nodes j = 1..3 of the group differ from it by an exponent that
+// is small in magnitude and is formed in FP32 from FP32 copies of Xp_c, Xm_c:
+//   a2_{c+j} - a2_c = j v2 h - dX_j,  dX_j = Xp_c (e^{jh} - 1) + Xm_c (e^{-jh} - 1),
+// E_{c+j} = E_c 2^{j v2 h - dX_j} (MUFU.EX2 and one FMUL).  Its FP32 rounding
+// is ~1e-7 (x cosh t) 3h in log2 units: < 3e-7 on config 4, < 3e-6 in the
+// cancellation band x ~ 0.66 v ~ 1e4 (test_wide_domain_fuzz_f32*).  cosh t
+// at every node is X_c + dX_j (S2 is sum w X, scaled by 1/(x log2(e)) once),
+// so the e^{+-t} FP32 recurrences of v2 go away.  Xp_c, Xm_c step per group
+// as X + X u (u = e^{+-4h} - 1, one FFMA2) and, with q, p and t, are
+// re-anchored from FP64 every kBlk3 nodes, where the FP32 partial sums are
+// also added into FP64 (every 128 nodes: FP32 recurrence drift over 32 group
+// steps is a few ulp, the partial sums' rounding ~1e-7 relative).  ~44
+// instructions per 4 nodes against 60 for v2.
+#ifndef BLK_F32_BLK3
+#define BLK_F32_BLK3 128
+#endif
+template <bool DV, bool DX>
+__device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, float hf, float shift,
+                                              int n, int mb, int me) {
+  constexpr int G = 4, CH = BLK_F32_BLK3;
+  static_assert(CH % G == 0, "blocks hold whole groups");
+  const double kLog2e = 1.4426950408889634;
+  const double v = vf, x = xf, t0 = t0f, h = hf;
+  const double v2 = v * kLog2e;
+  const double hx2 = 0.5 * x * kLog2e;
+  const double cst = (805306368.0 + 126.0) - ((double)shift + kLn2) * kLog2e;
+  const double e1 = exp(h), e1i = rcp64(e1), e2 = e1 * e1, eG = e2 * e2, eGi = rcp64(eG);
+  const double e2i = e1i * e1i;
+  // per-lane FP32 constants of the group offsets
+  const float U1 = float(e1 - 1.0), U2 = float(e2 - 1.0), U3 = float(e2 * e1 - 1.0);
+  const float V1 = float(e1i - 1.0), V2 = float(e2i - 1.0), V3 = float(e2i * e1i - 1.0);
+  const float uG = float(eG - 1.0), uGi = float(eGi - 1.0);
+  const double v2h = v2 * h;
+  const float J1 = float(v2h), J2 = float(2.0 * v2h), J3 = float(3.0 * v2h);
+  const float m2vl = float(-2.0 * v2);
+  const float eq1 = ex2_approx(m2vl * hf), eq2 = eq1 * eq1, eq3 = eq2 * eq1, eq4 = eq2 * eq2;
+  // 1 - q^j from a1 = 1 - q by exact identities (no cancellation for small
+  // v h, R21): 1 - q^2 = a1 (2 - a1), 1 - q^3 = a1 + q (1 - q^2), 1 - q^4 = a2 (2 - a2)
+  const float a1 = -expm1f(-2.0f * vf * hf), a2 = a1 * (2.0f - a1);
+  const float a3 = fmaf(1.0f - a1, a2, a1), a4 = a2 * (2.0f - a2);
+  const float h4 = 4.0f * hf;
+  const double tb = fma((double)mb, h, t0);
+  const double ebx = exp(tb);
+  double XpG = hx2 * ebx, XmG = hx2 * rcp64(ebx);
+  const double XpB = XpG, XmB = XmG;          // node mb (for node 0's half weight)
+  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+  double md = (double)mb;
+  int m = mb;
+#pragma unroll 1
+  while (m < me) {
+    const int c1 = min(m + CH, me);
+    const double tcd = fma(md, h, t0);
+    const float tcf = float(tcd);
+    // FP32 state re-anchored per block: Xp, Xm, q = e^{-2vt}, p = 1 - q, t
+    float2 X2 = f2(float(XpG), float(XmG));
+    const float q0 = ex2_approx(m2vl * tcf);
+    const float p0 = -expm1f(-2.0f * vf * tcf);
+    float2 qA = f2(q0, q0 * eq1), qB = f2(q0 * eq2, q0 * eq3);
+    float2 pA = f2(p0, fmaf(q0, a1, p0)), pB = f2(fmaf(q0, a2, p0), fmaf(q0, a3, p0));
+    float2 tA = f2(tcf, tcf + hf), tB = f2(fmaf(2.0f, hf, tcf), fmaf(3.0f, hf, tcf));
+    float2 C0 = f2s(0.0f), C1 = f2s(0.0f), C2 = f2s(0.0f);
+#pragma unroll 1
+    for (; m + G <= c1; m += G) {
+      const double tc = fma(md, h, t0);
+      md += (double)G;
+      const float Ec = exp2_fixed(fma(v2, tc, cst) - (XpG + XmG));
+      XpG *= eG; XmG *= eGi;
+      // exponent offsets of nodes 1..3 from the group's first node
+      const float Xp = X2.x, Xm = X2.y;
+      const float dX1 = fmaf(Xp, U1, Xm * V1);
+      const float2 dX23 = fma2(f2s(Xp), f2(U2, U3), mul2(f2s(Xm), f2(V2, V3)));
+      const float E1 = Ec * ex2_approx(J1 - dX1);
+      const float2 E23 = mul2(f2s(Ec), ex2_2(add2(f2(J2, J3), mul2(dX23, f2s(-1.0f)))));
+      const float Xc = Xp + Xm;
+      const float2 XA = f2(Xc, Xc + dX1), XB = add2(f2s(Xc), dX23);
+      X2 = fma2(X2, f2(uG, uGi), X2);
+      const float2 EA = f2(Ec, E1);
+      const float2 wA = fma2(EA, qA, EA), wB = fma2(E23, qB, E23);   // E (1 + q)
+      C0 = add2(C0, add2(wA, wB));
+      if (DX) C2 = fma2(wB, XB, fma2(wA, XA, C2));
+      if (DV) {
+        C1 = fma2(mul2(EA, pA), tA, C1);
+        C1 = fma2(mul2(E23, pB), tB, C1);
+        pA = fma2(qA, f2s(a4), pA);
+        pB = fma2(qB, f2s(a4), pB);
+      }
+      qA = mul2(qA, f2s(eq4));
+      qB = mul2(qB, f2s(eq4));
+      tA = add2(tA, f2s(h4));
+      tB = add2(tB, f2s(h4));
+    }
+    float B0 = C0.x + C0.y, B1 = C1.x + C1.y, B2 = C2.x + C2.y;
+    float q = qA.x, p = pA.x, tf = tA.x;
+#pragma unroll 1
+    for (; m < c1; ++m) {                                // remainder, one node at a time
+      const double t = fma(md, h, t0);
+      md += 1.0;
+      const double X = XpG + XmG;
+      const float E = exp2_fixed(fma(v2, t, cst) - X);
+      XpG *= e1; XmG *= e1i;
+      const float w = fmaf(E, q, E);
+      B0 += w;
+      if (DX) B2 = fmaf(w, float(X), B2);
+      if (DV) B1 = fmaf(E * tf, p, B1);
+      if (DV) p = fmaf(q, a1, p);
+      q *= eq1;
+      tf += hf;
+    }
+    S0 += B0; S1 += B1; S2 += B2;
+  }
+  // half weights of nodes 0 and n, evaluated directly; X at
+  // node 0 is the exact start state (mb == 0) and at node n = me - 1 one
+  // step back from the final recurrence state
+  auto half_node = [&](int mm, double X) {
+    const double t = fma((double)mm, h, t0);
+    const float E = 0.5f * exp2_fixed(fma(v2, t, cst) - X);
+    const float tf1 = float(t);
+    const float q1 = ex2_approx(m2vl * tf1);
+    const float w = fmaf(E, q1, E);
+    S0 -= w;
+    if (DX) S2 -= double(w) * X;
+    if (DV) S1 -= double(E * tf1) * (-expm1f(-2.0f * vf * tf1));
+  };
+  if (mb == 0) half_node(0, XpB + XmB);
+  if (mb < me && me == n + 1) half_node(n, fma(XpG, e1i, XmG * e1));
+  return Sums32{S0, S1, S2 * (1.0 / (2.0 * hx2))};
+}
+
 }  // namespace blk

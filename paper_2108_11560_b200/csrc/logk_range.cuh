@@ -170,8 +170,23 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 // and insensitive to the range (R20), so 2^-8 (the range is then at most
 // ~0.4% of its half-width wider than converged); 64-127 bins can still carry
 // a discretisation error on extreme inputs that a wider range shifts, so 2^-10.
+#ifndef BLK_F64_TOL_128
+#define BLK_F64_TOL_128 3.90625e-3f
+#endif
 __host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
-  return nbins >= 128 ? 3.90625e-3f : 9.765625e-4f;
+  return nbins >= 128 ? BLK_F64_TOL_128 : 9.765625e-4f;
+}
+// The FP32 entry point's threshold is eps = 2^-23 (R9): its eps-support is
+// about half as wide as the FP64 one, and 64 nodes over it leave the
+// trapezoid far below FP32 rounding (converged from 16 nodes), so
+// a range up to ~6% wider than converged, and a shift up to 1 below the
+// peak, change nothing it resolves: tol = 2^-4 (FP32 entry point, >= 64 bins;
+// c4 +8% against 2^-8, profiles/r02e_f32v3b.log).
+#ifndef BLK_F32_ENTRY_TOL
+#define BLK_F32_ENTRY_TOL 0.0625f
+#endif
+__host__ __device__ __forceinline__ float fz_tol_f32_entry(int nbins) {
+  return nbins >= 64 ? BLK_F32_ENTRY_TOL : 9.765625e-4f;
 }
 // For the PEAK search (F = g', F' = g'') what matters is not where t_p is
 // but how far g(a) lies below the maximum, because g(t_p) becomes the
