@@ -158,61 +158,62 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 
 // Alg. 2 with the two evaluations packed into f32x2 operations.  The loop
 // ends after max_iter = 10 iterations or earlier, per the paper's
-// "until" clause, once the Newton correction from the kept end a is
-// below kFzTolRel of |a|: a is then within that distance of the zero and
-// still on its outer side (F(a) < 0 is kept invariant), so the range stays
-// conservative; it is at most ~2^-10 relative wider than after 10 iterations,
-// which changes no output beyond rounding (R4, R20).  The literal
-// tol = 1 on |a_i - a_{i-1}| is not used (R4: it stops on the first
-// iteration that keeps a, and breaks config 3).
-// The tolerance follows the grid (the FP32 finder only runs from 64 bins on,
-// kF32PlanMinBins): from nbins = 128 the trapezoid error is at rounding level
-// and insensitive to the range (R20), so 2^-8 (the range is then at most
-// ~0.4% of its half-width wider than converged); 64-127 bins can still carry
-// a discretisation error on extreme inputs that a wider range shifts, so 2^-10.
-#ifndef BLK_F64_TOL_128
-#define BLK_F64_TOL_128 3.90625e-3f
+// "until" clause, on a working tolerance in log units (R4; the
+// literal tol = 1 on |a_i - a_{i-1}| stops on the first iteration that keeps
+// a and breaks config 3):
+//   * range ends (F = d = g - g_p - log eps): once the kept end a -- still on
+//     the outer side, F(a) < 0 is invariant -- has F(a) >= -end_nats, i.e.
+//     the integrand there is at least e^-end_nats of the eps level.  The
+//     range is then conservative and wider than the exact one by end_nats /
+//     |g'| at each end (~end_nats/36 of the half-width for a quadratic peak).
+//     (A test on the Newton correction relative to |a - t_p| instead would
+//     stop AT FindRange's end where d grows like x cosh t: there F/F' ~ 1 is
+//     small against the probe distance, leaving ranges many times too wide.)
+//   * the peak (F = g', F' = g''): what matters is not where t_p is but how
+//     far g(a) lies below the maximum, because g(t_p) becomes the log-sum-exp
+//     shift and the base of the eps threshold: Newton's estimate of that gap
+//     is F(a)^2 / (2 |F'(a)|), and the search stops once it is below
+//     peak_gap.  (A relative criterion on t_p would leave gaps of
+//     |g''| (tol t_p)^2 / 2 -- over 100 for x ~ 1e-30 and v ~ 1e4.)
+// The tolerances follow the grid (the FP32 finder only runs from 64 bins,
+// kF32PlanMinBins).  From 128 bins the FP64 trapezoid is insensitive to the
+// range -- widening the ends by 50% changes no output beyond 7e-14 (SURVEY
+// A.4) -- so end_nats = 4, peak_gap = 2 (the ends then lie at most ~6 nats
+// beyond the eps level, ~17% of the half-width): c3 +3.6%, c2 +3.4%, c5
+// +2.1% against the relative 2^-8 rule, outputs unchanged to rounding
+// (profiles/r02g_endnats.log); 64-127 bins can still carry a discretisation
+// error on extreme inputs that a wider range shifts, so 0.1 and 1/64.  The
+// FP32 entry point's threshold is eps = 2^-23 (R9), an eps-support about
+// half as wide, over which 64 nodes leave the trapezoid far below FP32
+// rounding (converged from 16 nodes): 4 and 2 from 64 bins (c4
+// +10%).
+struct FzTol {
+  float end_nats;   // range ends: stop once F(a) >= -end_nats
+  float peak_gap;   // peak: stop once F^2 / (2|F'|) <= peak_gap
+};
+#ifndef BLK_END_NATS_128
+#define BLK_END_NATS_128 4.0f
 #endif
-__host__ __device__ __forceinline__ float fz_tol_for(int nbins) {
-  return nbins >= 128 ? BLK_F64_TOL_128 : 9.765625e-4f;
-}
-// The FP32 entry point's threshold is eps = 2^-23 (R9): its eps-support is
-// about half as wide as the FP64 one, and 64 nodes over it leave the
-// trapezoid far below FP32 rounding (converged from 16 nodes), so
-// a range up to ~6% wider than converged, and a shift up to 1 below the
-// peak, change nothing it resolves: tol = 2^-4 (FP32 entry point, >= 64 bins;
-// c4 +8% against 2^-8, profiles/r02e_f32v3b.log).
-#ifndef BLK_F32_ENTRY_TOL
-#define BLK_F32_ENTRY_TOL 0.0625f
+#ifndef BLK_PEAK_GAP_128
+#define BLK_PEAK_GAP_128 2.0f
 #endif
-__host__ __device__ __forceinline__ float fz_tol_f32_entry(int nbins) {
-  return nbins >= 64 ? BLK_F32_ENTRY_TOL : 9.765625e-4f;
+__host__ __device__ __forceinline__ FzTol fz_tol_for(int nbins) {
+  return nbins >= 128 ? FzTol{BLK_END_NATS_128, BLK_PEAK_GAP_128} : FzTol{0.1f, 0.015625f};
 }
-// For the PEAK search (F = g', F' = g'') what matters is not where t_p is
-// but how far g(a) lies below the maximum, because g(t_p) becomes the
-// log-sum-exp shift and the base of the eps threshold: Newton's estimate of
-// that gap is F(a)^2 / (2 |F'(a)|), and the search stops once it is below
-// 16 tol in log units (1/16 at the 2^-8 tier of 128+ bins, 1/64 at 64-127).
-// A relative criterion on t_p would leave gaps of |g''| (tol t_p)^2 / 2 --
-// over 100 in log units for x ~ 1e-30 and v ~ 1e4 (t_p ~ 78), enough to push
-// FP32 weights out of range, and 0.6 at 64 bins for v ~ 2500, x ~ 1e-6.
-constexpr float kPeakGapPerTol = 16.0f;
-// For the range ends the Newton correction is measured against the distance
-// of a from the peak t_p (`ref`), the scale of the half-range, not against
-// |a|: for a far peak (t_p ~ 14 with a half-range of 0.3) |a| would allow
-// steps of several percent of the range.
+__host__ __device__ __forceinline__ FzTol fz_tol_f32_entry(int nbins) {
+  return nbins >= 64 ? FzTol{BLK_END_NATS_128, BLK_PEAK_GAP_128} : FzTol{0.1f, 0.015625f};
+}
 template <bool PEAK, bool ASC, class PF>
 __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
-                                               float dFa, float b, float tol, float ref = 0.0f) {
+                                               float dFa, float b, FzTol tol) {
 #pragma unroll 2
   for (int i = 0; i < kMaxIter; ++i) {
-    // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
-    // carries no information and must not end the search)
     if (PEAK) {
-      if (Fa * Fa <= (2.0f * kPeakGapPerTol * tol) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
+      // (an overflowed F'(a) -- far FindRange probes at x cosh t > FP32_MAX --
+      // carries no information and must not end the search)
+      if (Fa * Fa <= (2.0f * tol.peak_gap) * fabsf(dFa) && fabsf(dFa) <= 3.0e38f) break;
     } else {
-      const float rhs = tol * fabsf((a - ref) * dFa);
-      if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
+      if (Fa >= -tol.end_nats) break;
     }
     float mid, tn;
     fz_points_f32<ASC>(a, Fa, dFa, b, mid, tn);
@@ -246,7 +247,7 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 // Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
 // is taken in double on the caller's inputs.
 __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps,
-                                                    float tol) {
+                                                    FzTol tol) {
   Plan<float> p;
   PlanF32 P;
   P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
@@ -263,10 +264,10 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   const float c = p.gp + P.L + float(kLn2);
   p.t0 = 0.0f;
   float d0 = -P.x - p.gp - P.L;                                    // d(0)
-  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp, tol, p.tp);
+  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp, tol);
   auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
   if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
-  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol, p.tp);
+  p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol);
   p.dmin = fminf(d0, Fh);
   p.ok = true;
   return p;
@@ -279,12 +280,11 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
 // rule as find_zero_f32<false, ASC>.
 template <class PF>
 __device__ __forceinline__ float find_zero_f32_rt(const PF &P, float c, float a, float &Fa,
-                                                  float dFa, float b, float tol, float ref,
+                                                  float dFa, float b, FzTol tol,
                                                   bool asc, bool active) {
 #pragma unroll 1
   for (int i = 0; active && i < kMaxIter; ++i) {
-    const float rhs = tol * fabsf((a - ref) * dFa);
-    if (fabsf(Fa) <= rhs && rhs <= 3.0e38f) break;
+    if (Fa >= -tol.end_nats) break;
     const float mid = fmaf(b - a, 0.5f, a);
     const float t = fmaf(-Fa, rcp_approx(dFa), a);
     const float tn = asc ? fmaxf(fminf(t, mid), a) : fminf(fmaxf(t, mid), a);
@@ -303,7 +303,7 @@ __device__ __forceinline__ float find_zero_f32_rt(const PF &P, float c, float a,
 // the latency of one of the two searches is saved, which is what bounds
 // small batches.  All lanes of the pair must be active.
 __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, double log_eps,
-                                                         float tol, bool odd) {
+                                                         FzTol tol, bool odd) {
   Plan<float> p;
   PlanF32 P;
   P.v = float(vd); P.x = float(xd); P.hx = 0.5f * P.x; P.v2 = P.v * P.v;
@@ -329,7 +329,7 @@ __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, 
   } else {                                                        // t0 from 0 (if needed)
     a = 0.0f; Fa = d0; dFa = 0.0f; b = p.tp; active = d0 <= 0.0f;
   }
-  a = find_zero_f32_rt(P, c, a, Fa, dFa, b, tol, p.tp, !odd, active);
+  a = find_zero_f32_rt(P, c, a, Fa, dFa, b, tol, !odd, active);
   // the two lanes of the pair, named explicitly: they may leave the search
   // loop at different iterations, and __shfl_xor_sync with this mask waits
   // for both (an __activemask() taken here could miss the partner)

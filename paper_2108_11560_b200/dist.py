@@ -1,12 +1,14 @@
 """Multi-GPU driver: contiguous sharding of the element batch, one process per
-GPU (torchrun), no collective on the data path (elements are independent,
-P:58).  torch.distributed (NCCL over NVLink/NVSwitch on B200, gloo in
-the CPU tests) is used only after the timed region:
+GPU (torchrun), no collective on the data path of log K (elements are
+independent).  torch.distributed (NCCL over NVLink/NVSwitch on
+B200, gloo in the CPU tests) is used only:
 
-  * ``max_over_ranks``   all_reduce(MAX) of a per-rank elapsed time;
-  * ``gather_samples``   collects the outputs at a set of GLOBAL element
-    indices on every rank (each index is owned by exactly one shard, so a SUM
-    all-reduce of the zero-padded per-rank pieces assembles them exactly).
+  * ``max_over_ranks``     all_reduce(MAX) of a per-rank elapsed time (bench);
+  * ``gather_samples``     all_gather of each rank's own outputs at a set of
+    GLOBAL element indices (for checking against the oracle);
+  * ``nig_loglik_sharded`` the one real exchange of any path: the five NIG
+    log-likelihood sums (40 bytes) all-reduced across ranks, enqueued on the
+    stream the kernels ran on, with no host synchronisation.
 
 ``run_sharded`` evaluates one rank's shard with a caller-supplied compute
 function (the CUDA entry point in production).
@@ -23,48 +25,90 @@ def shard_range(n: int, world: int, rank: int):
     return n * rank // world, n * (rank + 1) // world
 
 
+def _multi():
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+
+
 def max_over_ranks(value: float, device=None) -> float:
     import torch
     import torch.distributed as dist
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if _multi():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
-def allreduce_sum(t):
-    """Sum a small tensor (e.g. the 5 NIG log-likelihood sums) over all ranks in
-    place -- the one collective of the NIG path (NCCL over NVLink on B200)."""
+def allreduce_sum(t, stream=None):
+    """Sum a small tensor over all ranks in place.  For a CUDA tensor the
+    collective is enqueued on ``stream`` (default: the current stream) after
+    the work already there -- the kernels that produced ``t`` -- and the call
+    returns without synchronising the host (NCCL collectives are
+    asynchronous to the host; the next op on ``stream`` sees the sum)."""
+    import torch
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if not _multi():
+        return t
+    if t.is_cuda:
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(t.device)):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    else:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t
 
 
-def nig_loglik_sharded(y_local, alpha, beta, delta, mu, nbins=128):
-    """Per-rank NIG sums on this rank's shard (CUDA kernels), then all_reduce."""
-    import paper_2108_11560_b200 as blk
-    out = blk.nig_loglik(y_local, alpha, beta, delta, mu, nbins=nbins)
-    return allreduce_sum(out)
+def nig_loglik_sharded(y_local, alpha, beta, delta, mu, nbins=128, stream=None, compute=None):
+    """NIG log-likelihood sums (sum log p, d/d(alpha, beta, delta, mu)) of the
+    sample whose contiguous shard ``y_local`` this rank holds: per-rank sums by
+    the CUDA kernels (``compute`` overrides them -- tests only), then one
+    all-reduce of the five numbers on the same stream (no host sync).
+    Returns the summed 5-vector (device tensor for the CUDA path)."""
+    if compute is None:
+        import paper_2108_11560_b200 as blk
+        out = blk.nig_loglik(y_local, alpha, beta, delta, mu, nbins=nbins, stream=stream)
+    else:
+        out = compute(y_local, alpha, beta, delta, mu, nbins)
+    return allreduce_sum(out, stream=stream)
 
 
 def gather_samples(local: dict, lo: int, hi: int, global_idx, device=None) -> dict:
     """local: kind -> 1-D tensor holding this rank's shard [lo, hi).
-    Returns kind -> tensor of len(global_idx) (identical on every rank)."""
+    Returns kind -> float64 tensor of len(global_idx) on ``device``, the same
+    on every rank: each rank contributes the samples its shard owns
+    (all_gather of (count-padded) positions and values), no rank sends
+    anything it does not own."""
     import torch
     import torch.distributed as dist
     idx = np.asarray(global_idx, dtype=np.int64)
-    mine = (idx >= lo) & (idx < hi)
-    pos = torch.from_numpy(np.nonzero(mine)[0]).to(device)
-    loc = torch.from_numpy(idx[mine] - lo).to(device)
-    out = {}
-    for k, t in local.items():
-        buf = torch.zeros(idx.size, dtype=torch.float64, device=device)
-        if loc.numel():
-            buf[pos] = t[loc.to(t.device)].to(device=device, dtype=torch.float64)
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
-        out[k] = buf
+    mine = np.nonzero((idx >= lo) & (idx < hi))[0]
+    pos = torch.from_numpy(mine).to(device)
+    loc = torch.from_numpy(idx[mine] - lo)
+    kinds = sorted(local)
+    vals = torch.stack([local[k][loc.to(local[k].device)].to(device=device, dtype=torch.float64)
+                        for k in kinds]) if kinds else torch.empty(0, device=device)
+    if not _multi():
+        out = {k: torch.zeros(idx.size, dtype=torch.float64, device=device) for k in kinds}
+        for r, k in enumerate(kinds):
+            out[k][pos] = vals[r]
+        return out
+    world = dist.get_world_size()
+    cnt = torch.tensor([mine.size], dtype=torch.int64, device=device)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt)
+    cmax = int(max(int(c.item()) for c in cnts))
+    ppos = torch.full((cmax,), -1, dtype=torch.int64, device=device)
+    ppos[:mine.size] = pos
+    pval = torch.zeros((len(kinds), cmax), dtype=torch.float64, device=device)
+    pval[:, :mine.size] = vals
+    all_pos = [torch.empty_like(ppos) for _ in range(world)]
+    all_val = [torch.empty_like(pval) for _ in range(world)]
+    dist.all_gather(all_pos, ppos)
+    dist.all_gather(all_val, pval)
+    out = {k: torch.zeros(idx.size, dtype=torch.float64, device=device) for k in kinds}
+    for p, v, c in zip(all_pos, all_val, cnts):
+        c = int(c.item())
+        for r, k in enumerate(kinds):
+            out[k][p[:c]] = v[r, :c]
     return out
 
 

@@ -94,19 +94,20 @@ def plan_violations(v, x, plan, exact):
     return np.array(bad)
 
 
-def plan_check_f32(v, x, plan, exact, tol):
+def plan_check_f32(v, x, plan, exact, end_nats, peak_gap):
     """The FP32 range finder's plan (BLK_RANGE_AUTO from 64 bins): Alg. 1-2 in
-    FP32, FindZero ending on the paper's "until" clause at a working
-    tolerance (R4) -- for the peak once Newton's estimate of the gap below
-    the maximum is < 16 tol -- all capped at 10 iterations.  Valid when
+    FP32, FindZero ending on the paper's "until" clause at working
+    tolerances in log units (R4) -- an end once F(a) >= -end_nats, the peak
+    once Newton's estimate of the gap below the maximum F^2/(2|F'|) is below
+    peak_gap -- all capped at 10 iterations.  Valid when
       * the shift is at or below the exact peak value, by at most
-        max(32 tol, |g''(t_p*)| (W0 2^-10)^2 / 2) (the stopping rule on
-        Newton's gap estimate, 16 tol, with 2x slack, or the 10-iteration
-        bracket) plus e_d;
+        max(2 peak_gap, |g''(t_p*)| (W0 2^-10)^2 / 2) (the stopping rule with
+        2x slack on Newton's estimate, or the 10-iteration bracket) plus e_d;
       * each range end lies on the outer side of the root of its OWN
         threshold g(t) = g_p + log eps (so also of the exact eps-support,
-        g_p <= g(t_p*)), within max(2 tol |t - t_p*|, W0 2^-10) + e_d / |g'|
-        of it (the stopping rule, or the 10-iteration bracket when Alg. 2's
+        g_p <= g(t_p*)), where d = g - g_p - log eps >= -end_nats - e_d (the
+        stopping rule) or within W0 2^-10 + e_d / |g'| of it (the
+        10-iteration bracket when Alg. 2's
         preference for the bisection point keeps Newton from converging --
         e.g. t1 for large x: bisection steps 2 -> 1 -> ... -> 0.0317 against
         the root 0.03125 after 10 iterations);
@@ -131,9 +132,7 @@ def plan_check_f32(v, x, plan, exact, tol):
             g2 = abs(float(vv * vv / mpmath.cosh(vv * tps) ** 2 - xx * mpmath.cosh(tps)))
             e_p = 2.0 ** -20 * (abs(gp) + float(x[i]) * float(mpmath.cosh(tps)) + float(v[i]) * tp_s + 40.0)
             gap = float(gstar) - gp
-            # the stopping rule bounds Newton's gap estimate F^2/(2|F'|) by 16 tol
-            # (2x slack for the estimate), or the 10-iteration bracket ends it
-            out = gap < -e_p or gap > max(32 * tol, g2 * (w_tp * 2.0 ** -10) ** 2 / 2) + e_p
+            out = gap < -e_p or gap > max(2 * peak_gap, g2 * (w_tp * 2.0 ** -10) ** 2 / 2) + e_p
 
             def d(t):
                 return g(t) - mpmath.mpf(gp) - L
@@ -153,8 +152,10 @@ def plan_check_f32(v, x, plan, exact, tol):
                 ed = 2.0 ** -20 * (abs(gp) + float(x[i]) * float(mpmath.cosh(ts)) + float(v[i]) * float(ts) + 40.0)
                 res = ed / max(slope, 1e-300)
                 tsf = float(ts)
-                if side * (t - tsf) < -res or abs(t - tsf) > max(2 * tol * abs(tsf - tp_s),
-                                                                w0 * 2.0 ** -10) + res:
+                dt = float(d(mpmath.mpf(float(t))))         # own threshold function at the end
+                outer = side * (t - tsf) >= -res
+                near = dt >= -end_nats - ed or abs(t - tsf) <= w0 * 2.0 ** -10 + res
+                if not (outer and near):
                     out = True
             bad.append(out)
     return np.array(bad)

@@ -117,9 +117,9 @@ def check_on_plan(got, v, x, nbins, ctx, range_mode=0, pin=60, tol_d=None):
                                                            replace=False)]))
     exact = [mp_plan(v[i], x[i]) for i in idx]
     f32 = range_mode == 0 and nbins >= 64
-    if f32:
-        tol = 3.90625e-3 if nbins >= 128 else 9.765625e-4
-        bad = plan_check_f32(np.abs(v[idx]), x[idx], plan[idx], exact, tol)
+    if f32:   # the FP32 finder's tolerances (logk_range.cuh fz_tol_for)
+        end_nats, peak_gap = (4.0, 2.0) if nbins >= 128 else (0.1, 1.0 / 64)
+        bad = plan_check_f32(np.abs(v[idx]), x[idx], plan[idx], exact, end_nats, peak_gap)
     else:
         bad = plan_violations(np.abs(v[idx]), x[idx], plan[idx], exact)
     assert not bad.any(), (ctx, idx[bad][:5], v[idx][bad][:3], x[idx][bad][:3], plan[idx][bad][:2])

@@ -91,6 +91,11 @@ def _free_port():
     return p
 
 
+def _cpu_sums(y, a, b, d, m, nbins):
+    """CPU stand-in for the kernels' per-rank sums (test only): the oracle."""
+    return torch.from_numpy(onig.nig_terms(y, a, b, d, m, nbins).sum(axis=1))
+
+
 def _worker(rank, world, port, q):
     from paper_2108_11560_b200 import dist as bdist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -99,15 +104,16 @@ def _worker(rank, world, port, q):
     try:
         y = _sample(1000, 5)
         lo, hi = bdist.shard_range(y.size, world, rank)
-        # CPU stand-in for the kernel's per-rank sums (test only)
-        local = torch.from_numpy(onig.nig_terms(y[lo:hi], 2.0, 0.5, 1.5, 0.3).sum(axis=1))
-        tot = bdist.allreduce_sum(local)
+        tot = bdist.nig_loglik_sharded(y[lo:hi], 2.0, 0.5, 1.5, 0.3, compute=_cpu_sums)
         q.put((rank, tot.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_nig_allreduce():
+def test_gloo_nig_loglik_sharded():
+    """dist.nig_loglik_sharded at world size 2 over gloo: each rank's shard
+    sums, one all-reduce, the same 5-vector on both ranks equal to the
+    single-process sums."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -123,3 +129,22 @@ def test_gloo_nig_allreduce():
     for r in (0, 1):
         assert np.allclose(res[r], ref, rtol=1e-13, atol=1e-10)
     assert np.array_equal(res[0], res[1])
+
+
+@pytest.mark.gpu
+def test_nig_sharded_torchrun():
+    """dist.nig_loglik_sharded end to end under torchrun over every GPU of the
+    box (NCCL; world 1 on the one-GPU pool, 8 on a full node): per-rank CUDA
+    kernels on contiguous shards, the all-reduce on the kernels' stream, the
+    result against the oracle on the whole sample (tests/mgpu_nig_driver.py).
+    NCCL_DEBUG=INFO shows the communicator's ranks in the log."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    g = torch.cuda.device_count()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--local-addr",
+           "127.0.0.1", f"--nproc-per-node={g}", os.path.join(here, "mgpu_nig_driver.py")]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", NCCL_DEBUG="INFO")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert f"NIG OK world={g}" in r.stdout
