@@ -92,25 +92,15 @@ __device__ __forceinline__ bool element_plan_f64(double v, double x, int nbins, 
   return ok && isfinite(t1) && isfinite(gp) && t1 > t0;
 }
 
+// One element (or one lane of LPE) of the FP64 path after the exp table is
+// in shared memory: a1-a7 for (vraw, x), outputs stored by lane sub == 0.
 template <bool LOGK, bool DV, bool DX, int LPE>
-__global__ void __launch_bounds__(128, BLK_MINB)
-logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
-                double *__restrict__ logk, double *__restrict__ dlogk_dv,
-                double *__restrict__ dlogk_dx, int nbins, int range_mode) {
-  BLK_TL(0);
-  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t i = gtid / LPE;
-  const int sub = (int)(gtid % LPE);
-  const bool live = i < n_el;
-  // Lanes past the end still take part in the shuffles (full-warp masks).
-  // The input loads are issued before the table copy and its barrier, which
-  // hide their latency (it stalled every warp at its first use of x).
-  const double vraw = live ? vin[i] : 1.0;
-  const double x = live ? xin[i] : 1.0;
-  load_exp_table();
-  __syncthreads();
+__device__ __forceinline__ void f64_element(double vraw, double x, bool live, int sub, size_t i,
+                                            double *__restrict__ logk,
+                                            double *__restrict__ dlogk_dv,
+                                            double *__restrict__ dlogk_dx, int nbins,
+                                            int range_mode) {
   const double *tab = g_exp_tab;
-
   const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
   const double v = fabs(vraw);
   const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
@@ -143,6 +133,32 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   if (LOGK) logk[i] = ok ? gp + log_sum(h * s.S0) : nanv;
   if (DV) dlogk_dv[i] = ok ? sgn * (s.S1 * r) : nanv;
   if (DX) dlogk_dx[i] = ok ? -(s.S2 * r) : nanv;
+}
+
+// The FP64 kernel: one element per lane (or LPE lanes per element).  (Two to
+// eight elements per thread in sequence, amortising the table copy and the
+// block launch, measured 2-6% slower on c2/c3/c5: the block-by-block launch
+// staggers the XU-bound plan and the FP64-bound quadrature across warps,
+// profiles/r02j_ept.log.)
+template <bool LOGK, bool DV, bool DX, int LPE>
+__global__ void __launch_bounds__(128, BLK_MINB)
+logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
+                double *__restrict__ logk, double *__restrict__ dlogk_dv,
+                double *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  BLK_TL(0);
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = gtid / LPE;
+  const int sub = (int)(gtid % LPE);
+  const bool live = i < n_el;
+  // Lanes past the end still take part in the shuffles (full-warp masks).
+  // The input loads are issued before the table copy and its barrier, which
+  // hide their latency (it stalled every warp at its first use of x).
+  const double vraw = live ? vin[i] : 1.0;
+  const double x = live ? xin[i] : 1.0;
+  load_exp_table();
+  __syncthreads();
+  f64_element<LOGK, DV, DX, LPE>(vraw, x, live, sub, i, logk, dlogk_dv, dlogk_dx, nbins,
+                                 range_mode);
 }
 
 // Second derivatives in the same pass: the three
@@ -221,16 +237,11 @@ logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ 
 #define BLK_F32_MINB 5
 #endif
 template <bool LOGK, bool DV, bool DX, int LPE>
-__global__ void __launch_bounds__(128, BLK_F32_MINB)
-logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, size_t n_el,
-                float *__restrict__ logk, float *__restrict__ dlogk_dv,
-                float *__restrict__ dlogk_dx, int nbins, int range_mode) {
-  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t i = gtid / LPE;
-  const int sub = (int)(gtid % LPE);
-  const bool live = i < n_el;
-  const float vraw = live ? vin[i] : 1.0f;
-  const float x = live ? xin[i] : 1.0f;
+__device__ __forceinline__ void f32_element(float vraw, float x, bool live, int sub, size_t i,
+                                            float *__restrict__ logk,
+                                            float *__restrict__ dlogk_dv,
+                                            float *__restrict__ dlogk_dx, int nbins,
+                                            int range_mode) {
   const bool valid = (x > 0.0f) && isfinite(x) && isfinite(vraw);
   const float v = fabsf(vraw);
   const float sgn = (vraw < 0.0f) ? -1.0f : 1.0f;
@@ -277,6 +288,21 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
   if (LOGK) logk[i] = ok ? gp + logf(h) + logf(float(s.S0)) : nanv;
   if (DV) dlogk_dv[i] = ok ? sgn * float(s.S1 * r0) : nanv;
   if (DX) dlogk_dx[i] = ok ? -float(s.S2 * r0) : nanv;
+}
+
+template <bool LOGK, bool DV, bool DX, int LPE>
+__global__ void __launch_bounds__(128, BLK_F32_MINB)
+logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, size_t n_el,
+                float *__restrict__ logk, float *__restrict__ dlogk_dv,
+                float *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t i = gtid / LPE;
+  const int sub = (int)(gtid % LPE);
+  const bool live = i < n_el;
+  const float vraw = live ? vin[i] : 1.0f;
+  const float x = live ? xin[i] : 1.0f;
+  f32_element<LOGK, DV, DX, LPE>(vraw, x, live, sub, i, logk, dlogk_dv, dlogk_dx, nbins,
+                                 range_mode);
 }
 
 // ------------------------------------------------------------ microbenchmarks
