@@ -83,7 +83,7 @@ def test_guards_logk(prec, n, lanes, nbins):
     only = [Guarded(n, dt) for _ in range(3)]
     f(gv.t, gx.t, None, only[1].t, None, nbins=nbins, lanes_per_element=lanes)
     torch.cuda.synchronize()
-    assert only[1].all_written() and torch.equal(only[1].t, outs[1].t)
+    assert only[1].all_written() and torch.equal(only[1].t.nan_to_num(7.0), outs[1].t.nan_to_num(7.0))
     for o in (only[0], only[2]):
         assert o.guards_ok() and bool((o.t.cpu() == FILL[dt]).all())
 
