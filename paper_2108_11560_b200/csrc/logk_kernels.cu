@@ -101,9 +101,10 @@ __device__ __forceinline__ void f64_element(double vraw, double x, bool live, in
                                             double *__restrict__ dlogk_dx, int nbins,
                                             int range_mode) {
   const double *tab = g_exp_tab;
-  const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
+  const bool valid = valid_input(vraw, x);
   const double v = fabs(vraw);
-  const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
+  const long long vbits = __double_as_longlong(vraw);
+  const double sgn = (vbits < 0 && vbits != (long long)0x8000000000000000ULL) ? -1.0 : 1.0;  // v < 0 (-0 -> +1)
 
   // a2-a5: integration plan (t_p, g(t_p), t0, t1)
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;
@@ -179,9 +180,10 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   const double x = live ? xin[i] : 1.0;
   load_exp_table();
   __syncthreads();
-  const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
+  const bool valid = valid_input(vraw, x);
   const double v = fabs(vraw);
-  const double sgn = (vraw < 0.0) ? -1.0 : 1.0;
+  const long long vbits = __double_as_longlong(vraw);
+  const double sgn = (vbits < 0 && vbits != (long long)0x8000000000000000ULL) ? -1.0 : 1.0;  // v < 0 (-0 -> +1)
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;
   const bool ok = valid && element_plan_f64<LPE>(v, x, nbins, range_mode, sub, tp, gp, t0, t1, dmin);
   Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -221,7 +223,7 @@ logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ 
   load_exp_table();
   __syncthreads();
   if (i >= n_el) return;
-  const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
+  const bool valid = valid_input(vraw, x);
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;
   const bool ok = valid && element_plan_f64<1>(fabs(vraw), x, nbins, range_mode, 0, tp, gp, t0, t1, dmin);
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
@@ -249,7 +251,7 @@ __device__ __forceinline__ void f32_element(float vraw, float x, bool live, int 
   float t0 = 0.0f, t1 = 0.0f, gp = 0.0f, dmin = 0.0f;
   bool ok = false;
   if (valid) {
-    if (use_f32_plan(range_mode, nbins, v, x)) {
+    if (use_f32_plan_f32_entry(range_mode, nbins, v, x)) {
       const Plan<float> p =
           (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF32, fz_tol_f32_entry(nbins), sub & 1)
                      : make_plan_f32(v, x, kLogEpsF32, fz_tol_f32_entry(nbins));
@@ -285,7 +287,7 @@ __device__ __forceinline__ void f32_element(float vraw, float x, bool live, int 
   if (!live || sub != 0) return;
   const float nanv = __int_as_float(0x7fc00000);
   const double r0 = rcp64(s.S0);
-  if (LOGK) logk[i] = ok ? gp + logf(h) + logf(float(s.S0)) : nanv;
+  if (LOGK) logk[i] = ok ? gp + logf(float(double(h) * s.S0)) : nanv;
   if (DV) dlogk_dv[i] = ok ? sgn * float(s.S1 * r0) : nanv;
   if (DX) dlogk_dx[i] = ok ? -float(s.S2 * r0) : nanv;
 }

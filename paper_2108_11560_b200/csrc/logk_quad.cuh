@@ -909,6 +909,31 @@ __device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, flo
 // also added into FP64 (every 128 nodes: FP32 recurrence drift over 32 group
 // steps is a few ulp, the partial sums' rounding ~1e-7 relative).  ~44
 // instructions per 4 nodes against 60 for v2.
+// e^x for the FP32 entry point's FP64 recurrence states (x in [-700, 700]):
+// 2^(x log2 e) with n = rint by the 1.5 2^52 magic add, e^(f ln 2), |f| <= 1/2,
+// by its Taylor series to degree 11 (truncation < 3e-15 relative; the
+// reduction's rounding ~1e-16 |x|): ~16 FP64 operations against ~35
+// instructions and a slow-path branch for libdevice exp.  The recurrences it
+// seeds need ~1e-11 (the FP32 weights resolve ~1e-7 of an exponent <= 10^3).
+__device__ __forceinline__ double exp_seed64(double x) {
+  const double y = x * 1.4426950408889634;
+  const double M = 6755399441055744.0;
+  const double t = y + M;
+  const double f = (y - (t - M)) * 0.6931471805599453;
+  double p = fma(f, 1.0 / 39916800.0, 1.0 / 3628800.0);
+  p = fma(p, f, 1.0 / 362880.0);
+  p = fma(p, f, 1.0 / 40320.0);
+  p = fma(p, f, 1.0 / 5040.0);
+  p = fma(p, f, 1.0 / 720.0);
+  p = fma(p, f, 1.0 / 120.0);
+  p = fma(p, f, 1.0 / 24.0);
+  p = fma(p, f, 1.0 / 6.0);
+  p = fma(p, f, 0.5);
+  p = fma(p, f, 1.0);
+  p = fma(p, f, 1.0);
+  return __hiloint2double(__double2hiint(p) + (__double2loint(t) << 20), __double2loint(p));
+}
+
 #ifndef BLK_F32_BLK3
 #define BLK_F32_BLK3 128
 #endif
@@ -922,7 +947,7 @@ __device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, flo
   const double v2 = v * kLog2e;
   const double hx2 = 0.5 * x * kLog2e;
   const double cst = (805306368.0 + 126.0) - ((double)shift + kLn2) * kLog2e;
-  const double e1 = exp(h), e1i = rcp64(e1), e2 = e1 * e1, eG = e2 * e2, eGi = rcp64(eG);
+  const double e1 = exp_seed64(h), e1i = rcp64(e1), e2 = e1 * e1, eG = e2 * e2, eGi = rcp64(eG);
   const double e2i = e1i * e1i;
   // per-lane FP32 constants of the group offsets
   const float U1 = float(e1 - 1.0), U2 = float(e2 - 1.0), U3 = float(e2 * e1 - 1.0);
@@ -938,10 +963,12 @@ __device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, flo
   const float a3 = fmaf(1.0f - a1, a2, a1), a4 = a2 * (2.0f - a2);
   const float h4 = 4.0f * hf;
   const double tb = fma((double)mb, h, t0);
-  const double ebx = exp(tb);
+  const double ebx = exp_seed64(tb);
   double XpG = hx2 * ebx, XmG = hx2 * rcp64(ebx);
   const double XpB = XpG, XmB = XmG;          // node mb (for node 0's half weight)
   double S0 = 0.0, S1 = 0.0, S2 = 0.0;
+  float qn0 = 0.0f, pn0 = 0.0f;
+  bool n_done = false;
   double md = (double)mb;
   int m = mb;
 #pragma unroll 1
@@ -953,6 +980,7 @@ __device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, flo
     float2 X2 = f2(float(XpG), float(XmG));
     const float q0 = ex2_approx(m2vl * tcf);
     const float p0 = -expm1f(-2.0f * vf * tcf);
+    if (m == 0) { qn0 = q0; pn0 = p0; }        // node 0's q, p for its half weight
     float2 qA = f2(q0, q0 * eq1), qB = f2(q0 * eq2, q0 * eq3);
     float2 pA = f2(p0, fmaf(q0, a1, p0)), pB = f2(fmaf(q0, a2, p0), fmaf(q0, a3, p0));
     float2 tA = f2(tcf, tcf + hf), tB = f2(fmaf(2.0f, hf, tcf), fmaf(3.0f, hf, tcf));
@@ -994,7 +1022,9 @@ __device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, flo
       const double t = fma(md, h, t0);
       md += 1.0;
       const double X = XpG + XmG;
-      const float E = exp2_fixed(fma(v2, t, cst) - X);
+      // node n carries weight 1/2, applied here
+      n_done = (m == n);
+      const float E = exp2_fixed(fma(v2, t, cst) - X) * (n_done ? 0.5f : 1.0f);
       XpG *= e1; XmG *= e1i;
       const float w = fmaf(E, q, E);
       B0 += w;
@@ -1006,11 +1036,22 @@ __device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, flo
     }
     S0 += B0; S1 += B1; S2 += B2;
   }
-  // half weights of nodes 0 and n, evaluated directly; X at
-  // node 0 is the exact start state (mb == 0) and at node n = me - 1 one
-  // step back from the final recurrence state
-  auto half_node = [&](int mm, double X) {
-    const double t = fma((double)mm, h, t0);
+  // half weights of nodes 0 and n.  Node 0's is taken back here
+  // from the exact start state and the first block's q, p (its t is t0f);
+  // node n's was applied in the remainder loop when it ended there (always
+  // for one lane and n + 1 not a multiple of 4, e.g. n = 128), else it is
+  // taken back here, X one step back from the final recurrence state.
+  if (mb == 0) {
+    const double X = XpB + XmB;
+    const float E = 0.5f * exp2_fixed(fma(v2, t0, cst) - X);
+    const float w = fmaf(E, qn0, E);
+    S0 -= w;
+    if (DX) S2 -= double(w) * X;
+    if (DV) S1 -= double(E * t0f) * pn0;
+  }
+  if (mb < me && me == n + 1 && !n_done) {
+    const double X = fma(XpG, e1i, XmG * e1);
+    const double t = fma((double)n, h, t0);
     const float E = 0.5f * exp2_fixed(fma(v2, t, cst) - X);
     const float tf1 = float(t);
     const float q1 = ex2_approx(m2vl * tf1);
@@ -1018,9 +1059,7 @@ __device__ __forceinline__ Sums32 quad_f32_v3(float vf, float xf, float t0f, flo
     S0 -= w;
     if (DX) S2 -= double(w) * X;
     if (DV) S1 -= double(E * tf1) * (-expm1f(-2.0f * vf * tf1));
-  };
-  if (mb == 0) half_node(0, XpB + XmB);
-  if (mb < me && me == n + 1) half_node(n, fma(XpG, e1i, XmG * e1));
+  }
   return Sums32{S0, S1, S2 * (1.0 / (2.0 * hx2))};
 }
 

@@ -424,8 +424,19 @@ __device__ __forceinline__ Plan<double> make_plan_f64(double v, double x, double
 // Inputs for which the FP32 range finder is used under BLK_RANGE_AUTO:
 // e^t, x cosh t and g stay far inside FP32 range and the d(t) cancellation
 // error stays below ~0.1 in log units.
+// (for v, x >= 0 the IEEE bit patterns order like the values: compared as
+// 64-bit integers on the ALU, not as doubles on the FP64 pipe, which the other
+// warps' node loops keep busy -- a DSETP there waits for it)
 __device__ __forceinline__ bool f32_plan_domain(double v, double x) {
-  return x >= 1e-30 && x <= 1e4 && v <= 1e4;
+  const long long xb = __double_as_longlong(x), vb = __double_as_longlong(v);
+  return xb >= 0x39B4484BFEEBC2A0LL /* 1e-30 */ && xb <= 0x40C3880000000000LL /* 1e4 */ &&
+         vb <= 0x40C3880000000000LL;
+}
+// Input test of every kernel (R16): x > 0 finite and v finite, by integer
+// tests on the bit patterns (same reason as above).
+__device__ __forceinline__ bool valid_input(double v, double x) {
+  const long long xb = __double_as_longlong(x), vb = __double_as_longlong(v);
+  return xb > 0 && xb < 0x7FF0000000000000LL && (vb & 0x7FFFFFFFFFFFFFFFLL) < 0x7FF0000000000000LL;
 }
 
 // Below this many bins BLK_RANGE_AUTO also takes the FP64 range finder: a
@@ -437,6 +448,15 @@ constexpr int kF32PlanMinBins = 64;
 // The range finder BLK_RANGE_AUTO picks for one element.
 __device__ __forceinline__ bool use_f32_plan(int range_mode, int nbins, double v, double x) {
   return range_mode == 0 && nbins >= kF32PlanMinBins && f32_plan_domain(v, x);
+}
+// The FP32 entry point (eps = 2^-23, R9) resolves only FP32: from 16 nodes over
+// its eps-support the trapezoid error is below FP32 rounding for any
+// conservative range (<= 1.3e-6 from n = 16), so its FP32 range
+// finder serves from 16 bins (the 0.1-nat tier below 64), the FP64 one below.
+constexpr int kF32EntryPlanMinBins = 16;
+__device__ __forceinline__ bool use_f32_plan_f32_entry(int range_mode, int nbins, double v,
+                                                       double x) {
+  return range_mode == 0 && nbins >= kF32EntryPlanMinBins && f32_plan_domain(v, x);
 }
 
 }  // namespace blk
