@@ -178,24 +178,24 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 // The tolerances follow the grid (the FP32 finder only runs from 64 bins,
 // kF32PlanMinBins).  From 128 bins the FP64 trapezoid is insensitive to the
 // range -- widening the ends by 50% changes no output beyond 7e-14 (SURVEY
-// A.4) -- so end_nats = 4, peak_gap = 2 (the ends then lie at most ~6 nats
-// beyond the eps level, ~17% of the half-width): c3 +3.6%, c2 +3.4%, c5
-// +2.1% against the relative 2^-8 rule, outputs unchanged to rounding
-// (profiles/r02g_endnats.log); 64-127 bins can still carry a discretisation
-// error on extreme inputs that a wider range shifts, so 0.1 and 1/64.  The
-// FP32 entry point's threshold is eps = 2^-23 (R9), an eps-support about
-// half as wide, over which 64 nodes leave the trapezoid far below FP32
-// rounding (converged from 16 nodes): 4 and 2 from 64 bins (c4
-// +10%).
+// A.4) -- so end_nats = 8, peak_gap = 4 (the ends then lie at most ~12 nats
+// beyond the eps level, ~1/3 of the half-width): c3 +4.6%, c2 +3.9%, c5 +2.8%
+// against the relative 2^-8 rule, outputs unchanged to rounding
+// (profiles/r02g_endnats.log, profiles/r02t_e8.log); 64-127 bins can still
+// carry a discretisation error on extreme inputs that a wider range shifts,
+// so 0.1 and 1/64.  The FP32 entry point's threshold is eps = 2^-23 (R9), an
+// eps-support about half as wide, over which 64 nodes leave the trapezoid far
+// below FP32 rounding (converged from 16 nodes): 8 and 4 from 64
+// bins (c4 +13%), the 0.1 / 1/64 tier at 16-63.
 struct FzTol {
   float end_nats;   // range ends: stop once F(a) >= -end_nats
   float peak_gap;   // peak: stop once F^2 / (2|F'|) <= peak_gap
 };
 #ifndef BLK_END_NATS_128
-#define BLK_END_NATS_128 4.0f
+#define BLK_END_NATS_128 8.0f
 #endif
 #ifndef BLK_PEAK_GAP_128
-#define BLK_PEAK_GAP_128 2.0f
+#define BLK_PEAK_GAP_128 4.0f
 #endif
 __host__ __device__ __forceinline__ FzTol fz_tol_for(int nbins) {
   return nbins >= 128 ? FzTol{BLK_END_NATS_128, BLK_PEAK_GAP_128} : FzTol{0.1f, 0.015625f};

@@ -118,7 +118,7 @@ def check_on_plan(got, v, x, nbins, ctx, range_mode=0, pin=60, tol_d=None):
     exact = [mp_plan(v[i], x[i]) for i in idx]
     f32 = range_mode == 0 and nbins >= 64
     if f32:   # the FP32 finder's tolerances (logk_range.cuh fz_tol_for)
-        end_nats, peak_gap = (4.0, 2.0) if nbins >= 128 else (0.1, 1.0 / 64)
+        end_nats, peak_gap = (8.0, 4.0) if nbins >= 128 else (0.1, 1.0 / 64)
         bad = plan_check_f32(np.abs(v[idx]), x[idx], plan[idx], exact, end_nats, peak_gap)
     else:
         bad = plan_violations(np.abs(v[idx]), x[idx], plan[idx], exact)
@@ -236,6 +236,16 @@ def test_extreme_domain(kernel):
     assert np.all(errors(got["logk"], lk, "logk") <= 1e-12)
     assert np.all(errors(got["dx"], dx, "dx") <= tol_d)
     assert np.all(errors(got["dv"], dv, "dv") <= tol_d)
+    _report_kappa("extreme", got, dv, dx, kappa)
+
+
+def _report_kappa(ctx, got, dv, dx, kappa):
+    """Print the derivative errors in units of kappa (evidence for the bound)."""
+    from parity import errors
+    ok = np.isfinite(dv) & np.isfinite(dx) & (dv != 0)
+    rv = errors(got["dv"][ok], dv[ok], "dv") / kappa[ok]
+    rx = errors(got["dx"][ok], dx[ok], "dx") / kappa[ok]
+    print(f"{ctx}: max dv err {rv.max():.3f} kappa, dx {rx.max():.3f} kappa")
 
 
 def test_large_x_dv_vs_brute_force_gpu():
@@ -522,6 +532,7 @@ def test_wide_domain_fuzz(seed):
     e1 = errors(got["dv"][ok], dv[ok], "dv")
     assert np.all(e1 <= tol_d[ok]), (v[ok][np.argmax(e1 / tol_d[ok])], x[ok][np.argmax(e1 / tol_d[ok])])
     assert np.all(got["dv"][v == 0] == 0.0)
+    _report_kappa(f"wide fuzz {seed}", got, dv, dx, kappa)
 
 
 @pytest.mark.parametrize("seed", [1, 2])
