@@ -223,15 +223,18 @@ def test_extreme_domain(kernel):
     and v t, so in double both the oracle and the kernel carry an absolute
     error ~eps * (x + v t_p) in every weight (tolerance note).
     For the five configs that is < 3e-12 and the north_star tolerances apply
-    unchanged; for x = 1e8 the oracle itself is 1.4e-9 from the exact dv
-    (tests/test_oracle_pins.py pins it to the brute force), so the derivative
-    tolerance here is max(1e-10, 10 * eps * (x + v t_p))."""
+    unchanged; beyond them kappa = eps (x + v t_p + 40) is the floor of any
+    double evaluation -- at x = 1e8 the oracle's dv is 1.4e-9 from the exact
+    value, and test_oracle_pins.py::test_large_x_dv_vs_brute_force pins it
+    within 0.5 kappa of the long-double brute force -- so the derivative
+    tolerance here is max(1e-10, 5 kappa).  Measured against the oracle: <= 0.05
+    kappa here, <= 1.96 kappa on the wide-domain fuzz (profiles/r02x_kappa.log)."""
     v = np.array([0, 0, 5, 0, 10, 2000, 5000, 1e4, 0.5, 5, 0, 30.0, 2e4, 3.0])
     x = np.array([1e3, 1e4, 1e5, 1e6, 1e8, 1e-3, 1e-4, 1e-2, 1e-6, 1e-10, 1e-8, 1e-30, 1.0, 1e-40])
     got = run_gpu(v, x, kernel=kernel)
     lk, dv, dx, plan = oracle.logk(v, x, NB, with_plan=True)
     kappa = np.finfo(float).eps * (x + v * plan[:, 0] + 40.0)
-    tol_d = np.maximum(1e-10, 10 * kappa)
+    tol_d = np.maximum(1e-10, 5 * kappa)
     from parity import errors
     assert np.all(errors(got["logk"], lk, "logk") <= 1e-12)
     assert np.all(errors(got["dx"], dx, "dx") <= tol_d)
@@ -240,19 +243,19 @@ def test_extreme_domain(kernel):
 
 
 def _report_kappa(ctx, got, dv, dx, kappa):
-    """Print the derivative errors against the bound max(1e-10, 10 kappa): in
+    """Print the derivative errors against the bound max(1e-10, 5 kappa): in
     units of kappa where the kappa term is the larger one, as relative errors
     elsewhere (evidence for the bound)."""
     from parity import errors
     ok = np.isfinite(dv) & np.isfinite(dx) & (dv != 0)
-    big = ok & (10 * kappa > 1e-10)
+    big = ok & (5 * kappa > 1e-10)
     small = ok & ~big
     out = []
     for k, r in (("dv", dv), ("dx", dx)):
         e = errors(got[k], r, k)
         kb = (e[big] / kappa[big]).max() if big.any() else 0.0
         sr = e[small].max() if small.any() else 0.0
-        out.append(f"{k}: {kb:.3f} kappa where 10 kappa > 1e-10 ({big.sum()}), {sr:.1e} rel. elsewhere")
+        out.append(f"{k}: {kb:.3f} kappa where 5 kappa > 1e-10 ({big.sum()}), {sr:.1e} rel. elsewhere")
     print(f"{ctx}: " + "; ".join(out))
 
 
@@ -529,7 +532,7 @@ def test_wide_domain_fuzz(seed):
     lk, dv, dx, plan = oracle.logk(v, x, NB, with_plan=True, threads=8)
     from parity import errors
     kappa = np.finfo(float).eps * (x + np.abs(v) * plan[:, 0] + 40.0)
-    tol_d = np.maximum(1e-10, 10 * kappa)
+    tol_d = np.maximum(1e-10, 5 * kappa)
     assert np.array_equal(np.isnan(got["logk"]), np.isnan(lk))
     ok = ~np.isnan(lk)
     tol_l = np.maximum(1e-12, kappa[ok] / np.maximum(1.0, np.abs(lk[ok])))
@@ -612,7 +615,7 @@ def test_f64_far_out_extremes():
         assert np.array_equal(np.isnan(g), np.isnan(r))
     ok = ~np.isnan(lk)
     kappa = np.finfo(float).eps * (x + v * np.nan_to_num(plan[:, 0]) + 40.0)
-    tol_d = np.maximum(1e-10, 10 * kappa)
+    tol_d = np.maximum(1e-10, 5 * kappa)
     assert np.all(errors(got["logk"][ok], lk[ok], "logk") <= 1e-12)
     assert np.all(errors(got["dx"][ok], dx[ok], "dx") <= tol_d[ok])
     assert np.all(errors(got["dv"][ok], dv[ok], "dv") <= tol_d[ok])
@@ -651,14 +654,14 @@ def _wide_inputs(seed, n=6000):
 def _wide_tol_d(v, x, nbins):
     _, _, _, plan = oracle.logk(v, x, nbins, with_plan=True, threads=8)
     kappa = np.finfo(float).eps * (x + np.abs(v) * np.nan_to_num(plan[:, 0]) + 40.0)
-    return np.maximum(1e-10, 10 * kappa)
+    return np.maximum(1e-10, 5 * kappa)
 
 
 def _assert_wide(got, v, x, nbins):
     lk, dv, dx, plan = oracle.logk(v, x, nbins, with_plan=True, threads=8)
     from parity import errors
     kappa = np.finfo(float).eps * (x + np.abs(v) * plan[:, 0] + 40.0)
-    tol_d = np.maximum(1e-10, 10 * kappa)
+    tol_d = np.maximum(1e-10, 5 * kappa)
     ok = ~np.isnan(lk)
     assert np.array_equal(np.isnan(got["logk"]), ~ok)
     assert errors(got["logk"][ok], lk[ok], "logk").max() <= 1e-12
@@ -754,6 +757,6 @@ def test_large_order_cancellation(lanes):
     assert np.all(eb <= 2 * tol_l), ((eb / tol_l).max(), v[np.argmax(eb / tol_l)], x[np.argmax(eb / tol_l)])
     e0 = errors(got["logk"], lk, "logk")
     assert np.all(e0 <= 2.5 * tol_l), ((e0 / tol_l).max(), v[np.argmax(e0 / tol_l)])
-    tol_d = np.maximum(1e-10, 10 * kappa)
+    tol_d = np.maximum(1e-10, 5 * kappa)
     assert np.all(errors(got["dv"], dv, "dv") <= tol_d)
     assert np.all(errors(got["dx"], dx, "dx") <= tol_d)
