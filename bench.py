@@ -73,7 +73,9 @@ def parse():
     p.add_argument("--n", type=int, default=0, help="override elements per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--cpu-seconds", type=float, default=None,
+                   help="oracle seconds: the GPU arm's cpu_baseline (default 10), or per "
+                        "step of --impl reference (default: the run fits in ~2 minutes)")
     p.add_argument("--out", default="")
     p.add_argument("--weak", action="store_true",
                    help="every rank its own full batch (default: the one batch in N shards)")
@@ -251,7 +253,7 @@ def run_reference(args, rank, world):
         return
     cores, model = cpu_info()
     c = workloads.CONFIGS[args.config]
-    per_step = max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    per_step = args.cpu_seconds or max(1.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     rates = []
     n_used = n_el = 0
     for i in range(args.warmup + args.steps):
@@ -450,7 +452,7 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cores, model = cpu_info()
-        r, ns, secs, nel = oracle_rate(args.config, args.nbins, args.cpu_seconds, cores)
+        r, ns, secs, nel = oracle_rate(args.config, args.nbins, args.cpu_seconds or 10.0, cores)
         cpu = {"value": r, "unit": "evals/s", "cores": cores, "kind": "oracle",
                "sample": f"{ns} evaluations: the first {nel} elements of {args.config}, "
                          f"{ns // max(1, nel)} pass(es) ({secs:.1f} s, {cores} threads, {model})"}
