@@ -70,6 +70,9 @@ __device__ __forceinline__ void lane_bins(int n, int sub, int &mb, int &me) {
   me = min(mb + per, n + 1);
 }
 
+#ifndef BLK_SMART_F64
+#define BLK_SMART_F64 true
+#endif
 // a2-a5 for one canonical element (v >= 0, x > 0 finite) of the FP64 entry
 // point: the range finder BLK_RANGE_AUTO / BLK_RANGE_F64 selects (FP32 from
 // 64 bins inside its domain, else FP64 with the table exp, which needs
@@ -83,7 +86,7 @@ __device__ __forceinline__ bool element_plan_f64(double v, double x, int nbins, 
   bool ok;
   if (use_f32_plan(range_mode, nbins, v, x)) {
     const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
-                                     : make_plan_f32(v, x, kLogEpsF64, fz_tol_for(nbins));
+                                     : make_plan_f32<BLK_SMART_F64>(v, x, kLogEpsF64, fz_tol_for(nbins));
     ok = p.ok; tp = p.tp; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
   } else {
     const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);

@@ -205,7 +205,7 @@ __host__ __device__ __forceinline__ FzTol fz_tol_f32_entry(int nbins) {
 }
 template <bool PEAK, bool ASC, class PF>
 __device__ __forceinline__ float find_zero_f32(const PF &P, float c, float a, float &Fa,
-                                               float dFa, float b, FzTol tol) {
+                                               float &dFa, float b, FzTol tol) {
 #pragma unroll 2
   for (int i = 0; i < kMaxIter; ++i) {
     if (PEAK) {
@@ -245,7 +245,27 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 }
 
 // Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
-// is taken in double on the caller's inputs.
+// is taken in double on the caller's inputs.  SMART (the FP64 kernel
+// from 64 bins): the
+// brackets Alg. 2 starts from come from the shape of g instead of Alg. 1's
+// doubling from t_s (R5b) -- every bracket end is checked by
+// evaluating F, and Alg. 1 runs whenever a check fails, so the results are
+// ranges Alg. 2 could have returned from Alg. 1's brackets:
+//   peak: [0, t*], t* = asinh(v/x): g'(0) = 0 and g'(t*) = v (tanh(v t*) - 1) <= 0;
+//   t0:   a Newton step of d from t_p - dq (normally inside: the left flank is
+//         flatter than the quadratic model) lands outside next to the root
+//         (d is concave there), dq = sqrt(2 |log eps| / |g''(t_p)|);
+//   t1:   likewise from t_p + 0.7 dq (the right flank falls faster than the
+//         model), or t_p + 0.7 dq itself when it is already outside.
+// c3 +3.6%, c2 +1.5% (profiles/r02y_smart*.log); no gain for the FP32 entry
+// point, whose searches are already short at eps = 2^-23.
+#ifndef BLK_T1_FRAC
+#define BLK_T1_FRAC 0.7f
+#endif
+#ifndef BLK_T0_FRAC
+#define BLK_T0_FRAC 1.0f
+#endif
+template <bool SMART = false>
 __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps,
                                                     FzTol tol) {
   Plan<float> p;
@@ -255,18 +275,71 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   float lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0f;
+  float K = 0.0f;                  // |g''| at the peak (curvature for the range brackets)
+  auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
   if (vd * vd - xd > 0.0) {
-    auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
-    if (!find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
+    bool bracketed = false;
+    if (SMART) {
+      // t* = asinh(v/x) is always on the outer side of the peak:
+      // g'(t*) = v (tanh(v t*) - 1) <= 0, and for v t* >> 1 it is the peak to
+      // FP32 resolution.  [0, t*] brackets it (g'(0) = 0), so Alg. 2 starts
+      // from t* instead of Alg. 1's doubling (which it replaces, R5b).
+      const float z = P.v / P.x;
+      const float ts = z > 1e4f ? lg2_approx(2.0f * z) * PlanF32::kLn2f
+                                : lg2_approx(z + sqrtf(fmaf(z, z, 1.0f))) * PlanF32::kLn2f;
+      pf(ts, Fh, dFh);
+      if (Fh < 0.0f && isfinite(dFh)) { hi = ts; lo = 0.0f; bracketed = true; }
+    }
+    if (!bracketed && !find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
     p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo, tol);  // (t_e, t_s)
+    K = fabsf(dFh);
+  } else {
+    K = P.x - P.v2;                // -g''(0) in the monotone regime
   }
   p.gp = P.gval(p.tp);
   const float c = p.gp + P.L + float(kLn2);
+  auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
+  // half-width of the quadratic model g ~ g_p - K (t - t_p)^2 / 2 at the eps level
+  const float dq = sqrtf(-2.0f * P.L / K);
+  const bool smart = SMART && isfinite(dq) && dq > 0.0f && dq < 32.0f;
   p.t0 = 0.0f;
   float d0 = -P.x - p.gp - P.L;                                    // d(0)
-  if (d0 <= 0.0f) p.t0 = find_zero_f32<false, true>(P, c, 0.0f, d0, 0.0f, p.tp, tol);
-  auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
-  if (!find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
+  if (d0 <= 0.0f) {
+    float a = 0.0f, Fa = d0, dFa = 0.0f, b = p.tp;
+    if (smart && p.tp - BLK_T0_FRAC * dq > 0.0f) {
+      // the left flank is flatter than the model (g'' -> v^2 sech^2 - x cosh t
+      // rises towards 0), so t_p - dq is normally inside: one Newton step from
+      // it lands outside (d is concave, its tangent lies above it) next to the
+      // root, and [tz, t_p - dq] brackets the root for Alg. 2
+      const float tq = p.tp - BLK_T0_FRAC * dq;
+      float Fq, dFq;
+      df(tq, Fq, dFq);
+      if (Fq < 0.0f) { a = tq; Fa = Fq; dFa = dFq; }
+      else if (dFq > 0.0f) {
+        const float tz = fmaxf(tq - Fq / dFq, 0.0f);
+        float Fz, dFz;
+        df(tz, Fz, dFz);
+        if (Fz < 0.0f) { a = tz; Fa = Fz; dFa = dFz; b = tq; }
+      }
+    }
+    p.t0 = find_zero_f32<false, true>(P, c, a, Fa, dFa, b, tol);
+    d0 = Fa;
+  }
+  bool bracketed = false;
+  if (smart) {
+    // the right flank falls faster than the model (x cosh t), so t_p + dq is
+    // normally outside; else a Newton step from it (inside) lands outside
+    const float tq = p.tp + BLK_T1_FRAC * dq;
+    df(tq, Fh, dFh);
+    if (Fh < 0.0f) { hi = tq; lo = p.tp; bracketed = true; }
+    else if (dFh < 0.0f) {
+      const float tz = tq - Fh / dFh;
+      float Fz, dFz;
+      df(tz, Fz, dFz);
+      if (Fz < 0.0f && isfinite(dFz)) { hi = tz; lo = tq; Fh = Fz; dFh = dFz; bracketed = true; }
+    }
+  }
+  if (!bracketed && !find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
   p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol);
   p.dmin = fminf(d0, Fh);
   p.ok = true;
