@@ -73,6 +73,9 @@ __device__ __forceinline__ void lane_bins(int n, int sub, int &mb, int &me) {
 #ifndef BLK_SMART_F64
 #define BLK_SMART_F64 true
 #endif
+#ifndef BLK_SMART_F32
+#define BLK_SMART_F32 true
+#endif
 // a2-a5 for one canonical element (v >= 0, x > 0 finite) of the FP64 entry
 // point: the range finder BLK_RANGE_AUTO / BLK_RANGE_F64 selects (FP32 from
 // 64 bins inside its domain, else FP64 with the table exp, which needs
@@ -257,7 +260,7 @@ __device__ __forceinline__ void f32_element(float vraw, float x, bool live, int 
     if (use_f32_plan_f32_entry(range_mode, nbins, v, x)) {
       const Plan<float> p =
           (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF32, fz_tol_f32_entry(nbins), sub & 1)
-                     : make_plan_f32(v, x, kLogEpsF32, fz_tol_f32_entry(nbins));
+                     : make_plan_f32<BLK_SMART_F32>(v, x, kLogEpsF32, fz_tol_f32_entry(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {
       const Plan<double> p = make_plan_f64(v, x, kLogEpsF32);

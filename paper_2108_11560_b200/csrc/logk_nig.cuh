@@ -20,6 +20,10 @@
 #include "logk_quad.cuh"
 #include "logk_range.cuh"
 
+#ifndef BLK_SMART_NIG
+#define BLK_SMART_NIG true
+#endif
+
 namespace blk {
 
 constexpr int kNigThreads = 128;
@@ -49,7 +53,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
       double t0, t1, gp, dmin;
       bool ok;
       if (use_f32_plan(0, nbins, 1.0, z)) {
-        const Plan<float> p = make_plan_f32(1.0, z, kLogEpsF64, fz_tol_for(nbins));
+        const Plan<float> p = make_plan_f32<BLK_SMART_NIG>(1.0, z, kLogEpsF64, fz_tol_for(nbins));
         ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
       } else {
         const Plan<double> p = make_plan_f64_tab(1.0, z, kLogEpsF64);

@@ -245,9 +245,9 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 }
 
 // Alg. 3 lines 2-9 in FP32.  The regime test g''(0) = v^2 - x > 0
-// is taken in double on the caller's inputs.  SMART (the FP64 kernel
-// from 64 bins): the
-// brackets Alg. 2 starts from come from the shape of g instead of Alg. 1's
+// is taken in double on the caller's inputs.  SMART (every kernel's
+// FP32 range finder): the brackets Alg. 2 starts from come from the shape of
+// g instead of Alg. 1's
 // doubling from t_s (R5b) -- every bracket end is checked by
 // evaluating F, and Alg. 1 runs whenever a check fails, so the results are
 // ranges Alg. 2 could have returned from Alg. 1's brackets:
@@ -257,8 +257,8 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 //         (d is concave there), dq = sqrt(2 |log eps| / |g''(t_p)|);
 //   t1:   likewise from t_p + 0.7 dq (the right flank falls faster than the
 //         model), or t_p + 0.7 dq itself when it is already outside.
-// c3 +3.6%, c2 +1.5% (profiles/r02y_smart*.log); no gain for the FP32 entry
-// point, whose searches are already short at eps = 2^-23.
+// c3 +9.9%, c2 +5.6%, c4 (FP32 entry point) +14% (profiles/r02y_smart*.log,
+// profiles/r02zb_peak.log).
 #ifndef BLK_T1_FRAC
 #define BLK_T1_FRAC 0.7f
 #endif
@@ -284,9 +284,12 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
       // g'(t*) = v (tanh(v t*) - 1) <= 0, and for v t* >> 1 it is the peak to
       // FP32 resolution.  [0, t*] brackets it (g'(0) = 0), so Alg. 2 starts
       // from t* instead of Alg. 1's doubling (which it replaces, R5b).
+      // (moved out by 2^-10 relative + 1e-4: where v t* >> 1, g'(t*) is below
+      // the FP32 rounding of its two ~v-sized terms and could test >= 0)
       const float z = P.v / P.x;
-      const float ts = z > 1e4f ? lg2_approx(2.0f * z) * PlanF32::kLn2f
+      const float ta = z > 1e4f ? lg2_approx(2.0f * z) * PlanF32::kLn2f
                                 : lg2_approx(z + sqrtf(fmaf(z, z, 1.0f))) * PlanF32::kLn2f;
+      const float ts = fmaf(ta, 1.0009765625f, 1e-4f);
       pf(ts, Fh, dFh);
       if (Fh < 0.0f && isfinite(dFh)) { hi = ts; lo = 0.0f; bracketed = true; }
     }
