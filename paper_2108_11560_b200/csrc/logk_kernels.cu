@@ -88,7 +88,7 @@ __device__ __forceinline__ bool element_plan_f64(double v, double x, int nbins, 
                                                  double &t1, double &dmin) {
   bool ok;
   if (use_f32_plan(range_mode, nbins, v, x)) {
-    const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
+    const Plan<float> p = (LPE >= 2) ? make_plan_f32_pair<BLK_SMART_F64>(v, x, kLogEpsF64, fz_tol_for(nbins), sub & 1)
                                      : make_plan_f32<BLK_SMART_F64>(v, x, kLogEpsF64, fz_tol_for(nbins));
     ok = p.ok; tp = p.tp; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
   } else {
@@ -259,7 +259,7 @@ __device__ __forceinline__ void f32_element(float vraw, float x, bool live, int 
   if (valid) {
     if (use_f32_plan_f32_entry(range_mode, nbins, v, x)) {
       const Plan<float> p =
-          (LPE >= 2) ? make_plan_f32_pair(v, x, kLogEpsF32, fz_tol_f32_entry(nbins), sub & 1)
+          (LPE >= 2) ? make_plan_f32_pair<BLK_SMART_F32>(v, x, kLogEpsF32, fz_tol_f32_entry(nbins), sub & 1)
                      : make_plan_f32<BLK_SMART_F32>(v, x, kLogEpsF32, fz_tol_f32_entry(nbins));
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     } else {

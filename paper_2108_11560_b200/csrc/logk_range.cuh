@@ -265,6 +265,67 @@ __device__ __forceinline__ bool find_range(const Fn &f, T ts, T &lo, T &hi, T &F
 #ifndef BLK_T0_FRAC
 #define BLK_T0_FRAC 1.0f
 #endif
+// R5b bracket helpers (see above).  Each returns whether its bracket was
+// established; the caller falls back to Alg. 1 otherwise.
+template <class PFN>
+__device__ __forceinline__ bool smart_peak_bracket(const PlanF32 &P, const PFN &pf, float &lo,
+                                                   float &hi, float &Fh, float &dFh) {
+  // t* = asinh(v/x) is always on the outer side of the peak:
+  // g'(t*) = v (tanh(v t*) - 1) <= 0, and for v t* >> 1 it is the peak to
+  // FP32 resolution.  [0, t*] brackets it (g'(0) = 0).  (t* is moved out by
+  // 2^-10 relative + 1e-4: where v t* >> 1, g'(t*) is below the FP32
+  // rounding of its two ~v-sized terms and could test >= 0.)
+  const float z = P.v / P.x;
+  const float ta = z > 1e4f ? lg2_approx(2.0f * z) * PlanF32::kLn2f
+                            : lg2_approx(z + sqrtf(fmaf(z, z, 1.0f))) * PlanF32::kLn2f;
+  const float ts = fmaf(ta, 1.0009765625f, 1e-4f);
+  pf(ts, Fh, dFh);
+  if (!(Fh < 0.0f && isfinite(dFh))) return false;
+  hi = ts; lo = 0.0f;
+  return true;
+}
+// t0: the left flank is flatter than the quadratic model (g'' -> v^2 sech^2 -
+// x cosh t rises towards 0), so t_p - dq is normally inside: one Newton step
+// from it lands outside (d is concave, its tangent lies above it) next to the
+// root, and [tz, t_p - dq] brackets the root for Alg. 2.
+template <class DFN>
+__device__ __forceinline__ void smart_t0_bracket(const DFN &df, float tp, float dq, float &a,
+                                                 float &Fa, float &dFa, float &b) {
+  const float tq = tp - BLK_T0_FRAC * dq;
+  if (!(tq > 0.0f)) return;
+  float Fq, dFq;
+  df(tq, Fq, dFq);
+  if (Fq < 0.0f) { a = tq; Fa = Fq; dFa = dFq; }
+  else if (dFq > 0.0f) {
+    const float tz = fmaxf(tq - Fq / dFq, 0.0f);
+    float Fz, dFz;
+    df(tz, Fz, dFz);
+    if (Fz < 0.0f) { a = tz; Fa = Fz; dFa = dFz; b = tq; }
+  }
+}
+// t1: the right flank falls faster than the model (x cosh t), so t_p + 0.7 dq
+// is outside or a Newton step from it (inside) lands outside.
+template <class DFN>
+__device__ __forceinline__ bool smart_t1_bracket(const DFN &df, float tp, float dq, float &lo,
+                                                 float &hi, float &Fh, float &dFh) {
+  const float tq = tp + BLK_T1_FRAC * dq;
+  df(tq, Fh, dFh);
+  if (Fh < 0.0f) { hi = tq; lo = tp; return true; }
+  if (dFh < 0.0f) {
+    const float tz = tq - Fh / dFh;
+    float Fz, dFz;
+    df(tz, Fz, dFz);
+    if (Fz < 0.0f && isfinite(dFz)) { hi = tz; lo = tq; Fh = Fz; dFh = dFz; return true; }
+  }
+  return false;
+}
+// half-width of the quadratic model g ~ g_p - K (t - t_p)^2 / 2 at the eps
+// level, when usable for the brackets (< 32 keeps every probe in FP32 range)
+__device__ __forceinline__ float model_halfwidth(float L, float K) {
+  const float dq = sqrtf(-2.0f * L / K);
+  return (isfinite(dq) && dq > 0.0f && dq < 32.0f) ? dq : 0.0f;
+}
+
 template <bool SMART = false>
 __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, double log_eps,
                                                     FzTol tol) {
@@ -275,25 +336,11 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   float lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0f;
-  float K = 0.0f;                  // |g''| at the peak (curvature for the range brackets)
+  float K;                         // |g''| at the peak (curvature for the range brackets)
   auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
   if (vd * vd - xd > 0.0) {
-    bool bracketed = false;
-    if (SMART) {
-      // t* = asinh(v/x) is always on the outer side of the peak:
-      // g'(t*) = v (tanh(v t*) - 1) <= 0, and for v t* >> 1 it is the peak to
-      // FP32 resolution.  [0, t*] brackets it (g'(0) = 0), so Alg. 2 starts
-      // from t* instead of Alg. 1's doubling (which it replaces, R5b).
-      // (moved out by 2^-10 relative + 1e-4: where v t* >> 1, g'(t*) is below
-      // the FP32 rounding of its two ~v-sized terms and could test >= 0)
-      const float z = P.v / P.x;
-      const float ta = z > 1e4f ? lg2_approx(2.0f * z) * PlanF32::kLn2f
-                                : lg2_approx(z + sqrtf(fmaf(z, z, 1.0f))) * PlanF32::kLn2f;
-      const float ts = fmaf(ta, 1.0009765625f, 1e-4f);
-      pf(ts, Fh, dFh);
-      if (Fh < 0.0f && isfinite(dFh)) { hi = ts; lo = 0.0f; bracketed = true; }
-    }
-    if (!bracketed && !find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
+    const bool br = SMART && smart_peak_bracket(P, pf, lo, hi, Fh, dFh);
+    if (!br && !find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
     p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo, tol);  // (t_e, t_s)
     K = fabsf(dFh);
   } else {
@@ -302,47 +349,17 @@ __device__ __forceinline__ Plan<float> make_plan_f32(double vd, double xd, doubl
   p.gp = P.gval(p.tp);
   const float c = p.gp + P.L + float(kLn2);
   auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
-  // half-width of the quadratic model g ~ g_p - K (t - t_p)^2 / 2 at the eps level
-  const float dq = sqrtf(-2.0f * P.L / K);
-  const bool smart = SMART && isfinite(dq) && dq > 0.0f && dq < 32.0f;
+  const float dq = SMART ? model_halfwidth(P.L, K) : 0.0f;
   p.t0 = 0.0f;
   float d0 = -P.x - p.gp - P.L;                                    // d(0)
   if (d0 <= 0.0f) {
     float a = 0.0f, Fa = d0, dFa = 0.0f, b = p.tp;
-    if (smart && p.tp - BLK_T0_FRAC * dq > 0.0f) {
-      // the left flank is flatter than the model (g'' -> v^2 sech^2 - x cosh t
-      // rises towards 0), so t_p - dq is normally inside: one Newton step from
-      // it lands outside (d is concave, its tangent lies above it) next to the
-      // root, and [tz, t_p - dq] brackets the root for Alg. 2
-      const float tq = p.tp - BLK_T0_FRAC * dq;
-      float Fq, dFq;
-      df(tq, Fq, dFq);
-      if (Fq < 0.0f) { a = tq; Fa = Fq; dFa = dFq; }
-      else if (dFq > 0.0f) {
-        const float tz = fmaxf(tq - Fq / dFq, 0.0f);
-        float Fz, dFz;
-        df(tz, Fz, dFz);
-        if (Fz < 0.0f) { a = tz; Fa = Fz; dFa = dFz; b = tq; }
-      }
-    }
+    if (dq > 0.0f) smart_t0_bracket(df, p.tp, dq, a, Fa, dFa, b);
     p.t0 = find_zero_f32<false, true>(P, c, a, Fa, dFa, b, tol);
     d0 = Fa;
   }
-  bool bracketed = false;
-  if (smart) {
-    // the right flank falls faster than the model (x cosh t), so t_p + dq is
-    // normally outside; else a Newton step from it (inside) lands outside
-    const float tq = p.tp + BLK_T1_FRAC * dq;
-    df(tq, Fh, dFh);
-    if (Fh < 0.0f) { hi = tq; lo = p.tp; bracketed = true; }
-    else if (dFh < 0.0f) {
-      const float tz = tq - Fh / dFh;
-      float Fz, dFz;
-      df(tz, Fz, dFz);
-      if (Fz < 0.0f && isfinite(dFz)) { hi = tz; lo = tq; Fh = Fz; dFh = dFz; bracketed = true; }
-    }
-  }
-  if (!bracketed && !find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
+  const bool br = dq > 0.0f && smart_t1_bracket(df, p.tp, dq, lo, hi, Fh, dFh);
+  if (!br && !find_range(df, p.tp, lo, hi, Fh, dFh)) return p;
   p.t1 = find_zero_f32<false, false>(P, c, hi, Fh, dFh, lo, tol);
   p.dmin = fminf(d0, Fh);
   p.ok = true;
@@ -378,6 +395,7 @@ __device__ __forceinline__ float find_zero_f32_rt(const PF &P, float c, float a,
 // shuffle.  Same ranges as make_plan_f32 (the same arithmetic per search);
 // the latency of one of the two searches is saved, which is what bounds
 // small batches.  All lanes of the pair must be active.
+template <bool SMART = false>
 __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, double log_eps,
                                                          FzTol tol, bool odd) {
   Plan<float> p;
@@ -387,23 +405,35 @@ __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, 
   float lo, hi, Fh, dFh;
   p.ok = false;
   p.tp = 0.0f;
+  float K;
+  bool peak_ok = true;
   if (vd * vd - xd > 0.0) {
     auto pf = [&](float t, float &F, float &dF) { P.peak1(t, F, dF); };
-    if (!find_range(pf, 0.0f, lo, hi, Fh, dFh)) return p;
-    p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo, tol);
+    const bool br = SMART && smart_peak_bracket(P, pf, lo, hi, Fh, dFh);
+    peak_ok = br || find_range(pf, 0.0f, lo, hi, Fh, dFh);
+    if (peak_ok) p.tp = find_zero_f32<true, false>(P, 0.0f, hi, Fh, dFh, lo, tol);
+    K = fabsf(dFh);
+  } else {
+    K = P.x - P.v2;
   }
+  // (both lanes of the pair reach the shuffles below, also on failure)
   p.gp = P.gval(p.tp);
   const float c = p.gp + P.L + float(kLn2);
   const float d0 = -P.x - p.gp - P.L;                             // d(0)
-  bool range_ok = true;
+  const float dq = SMART ? model_halfwidth(P.L, K) : 0.0f;
+  auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
+  bool range_ok = peak_ok;
   float a, Fa, dFa, b;
   bool active;
   if (odd) {                                                      // t1: FindRange first
-    auto df = [&](float t, float &F, float &dF) { P.thr1(c, t, F, dF); };
-    range_ok = find_range(df, p.tp, lo, hi, Fh, dFh);
+    if (range_ok) {
+      const bool br = dq > 0.0f && smart_t1_bracket(df, p.tp, dq, lo, hi, Fh, dFh);
+      range_ok = br || find_range(df, p.tp, lo, hi, Fh, dFh);
+    }
     a = hi; Fa = Fh; dFa = dFh; b = lo; active = range_ok;
   } else {                                                        // t0 from 0 (if needed)
-    a = 0.0f; Fa = d0; dFa = 0.0f; b = p.tp; active = d0 <= 0.0f;
+    a = 0.0f; Fa = d0; dFa = 0.0f; b = p.tp; active = range_ok && d0 <= 0.0f;
+    if (active && dq > 0.0f) smart_t0_bracket(df, p.tp, dq, a, Fa, dFa, b);
   }
   a = find_zero_f32_rt(P, c, a, Fa, dFa, b, tol, !odd, active);
   // the two lanes of the pair, named explicitly: they may leave the search
@@ -415,7 +445,7 @@ __device__ __forceinline__ Plan<float> make_plan_f32_pair(double vd, double xd, 
   const bool ok_o = __shfl_xor_sync(mask, (int)range_ok, 1) != 0;
   const float t0 = odd ? a_o : a, t1 = odd ? a : a_o;
   const float F0 = odd ? Fa_o : Fa, F1 = odd ? Fa : Fa_o;
-  if (!(odd ? range_ok : ok_o)) return p;
+  if (!peak_ok || !(odd ? range_ok : ok_o)) return p;
   p.t0 = (d0 <= 0.0f) ? t0 : 0.0f;
   p.t1 = t1;
   p.dmin = fminf(d0 <= 0.0f ? F0 : d0, F1);
