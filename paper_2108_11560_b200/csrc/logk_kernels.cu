@@ -276,13 +276,8 @@ __device__ __forceinline__ void f32_element(float vraw, float x, bool live, int 
     // the fixed-point exponent needs every node within 2^-126 of the peak:
     // true when both range ends are < 60 below the log-eps level (always on
     // ranges found by Alg. 1-3; kept exact for safety)
-#if defined(BLK_F32_V2)
-    if (dmin > -60.0f) s = quad_f32_v2<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
-    else
-#elif !defined(BLK_F32_V1)
     if (dmin > -60.0f) s = quad_f32_v3<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
     else
-#endif
       s = quad_f32<DV, DX>(v, x, t0, h, gp, nbins, mb, me);
   }
   if (LPE > 1) {

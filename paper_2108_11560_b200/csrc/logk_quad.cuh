@@ -16,8 +16,9 @@
 //   nodes_fp64     the general loop: p = 1 - q by an additive recurrence (no
 //                  cancellation for small vt, R21), e^{+-t} re-anchored every
 //                  kAnchor nodes, exp clamp for ranges far below eps;
-//   quad_f32_v2    FP32 entry point: FP64 exponent as a fixed-point number,
-//                  MUFU.EX2, FP32 f32x2 node pairs; quad_f32 its fallback.
+//   quad_f32_v3    FP32 entry point: one FP64 fixed-point exponent per 4
+//                  nodes, FP32 offsets and f32x2 node pairs, MUFU.EX2;
+//                  quad_f32 its fallback for ranges far below eps.
 // The half weights of the two end nodes are taken back outside
 // the loops, so the loop bodies carry no per-node select.
 #pragma once
@@ -754,20 +755,17 @@ __device__ __forceinline__ Sums32 quad_f32(float vf, float xf, float t0f, float 
   return Sums32{S0, S1, S2};
 }
 
-// FP32 entry point, fast path.  The weight exponent in log2 units,
+// FP32 entry point, fixed-point exponent.  The weight exponent in log2 units,
 // a2 = (v t - x cosh t - s - log 2) log2(e), is formed in FP64 as
 // A = a2 + 126 + M with M = 1.5 * 2^29 (ulp 2^-23), so the low word of A is
 // ((n + 126) << 23) | f for a2 = n + f/2^23 (n = floor(a2), two's complement).
 // Then 2^(a2) = 2^n * 2^(f/2^23) costs one LOP3 (the float 1.f), one MUFU.EX2
 // (2^(1.f) = 2 * 2^(f/2^23)) and one IADD3 on its bits: ex2 + lo - bits(1.f)
 // = bits(2^(f/2^23)) + (n << 23) -- no FP64->FP32 conversion, no shift.
-// FP64 work per node is the v2 recurrence of the FP64 loop (X = x cosh t
-// log2(e) = Xp + Xm, B = B_c + j v h log2(e) with M and the shift folded into
-// B_c): 4.75 operations, each with at most two register operands.  Needs
-// a2 in [-126, 128): the caller takes this path only when the range's end
-// points sit less than 60 (natural log) below the peak.  Quantisation of a2
-// to 2^-23 (plus two FP64 roundings at that scale) is <= 1.2e-7 relative in a
-// weight, below FP32 rounding.
+// Needs a2 in [-126, 128): the caller takes this path only when the range's
+// end points sit less than 60 (natural log) below the peak.  Quantisation of
+// a2 to 2^-23 (plus two FP64 roundings at that scale) is <= 1.2e-7 relative
+// in a weight, below FP32 rounding.
 __device__ __forceinline__ float exp2_fixed(double A) {
   const int lo = __double2loint(A);
   int fb;   // (lo & 0x007fffff) | 0x3f800000 as one LOP3 (lut 0xEA = (a & b) | c)
@@ -776,127 +774,10 @@ __device__ __forceinline__ float exp2_fixed(double A) {
   return __int_as_float(__float_as_int(e) + lo - fb);
 }
 
-template <bool DV, bool DX>
-__device__ __forceinline__ Sums32 quad_f32_v2(float vf, float xf, float t0f, float hf, float shift,
-                                              int n, int mb, int me) {
-  constexpr int G = 4, CH = 32;                 // nodes per group, per FP32 block
-  const double kLog2e = 1.4426950408889634;
-  const double v = vf, x = xf, t0 = t0f, h = hf;
-  const double v2 = v * kLog2e, v2h = v2 * h;
-  const double hx2 = 0.5 * x * kLog2e;         // X = hx2 (e^t + e^-t) = x cosh t log2(e)
-  const double cst = (805306368.0 + 126.0) - ((double)shift + kLn2) * kLog2e;
-  // e^{G h} by squaring: a few ulp of drift over n/G group steps is ~1e-14
-  // relative in X, far below what the FP32 weights resolve
-  const double e1 = exp(h), e1i = rcp64(e1), e2 = e1 * e1, eG = e2 * e2, eGi = rcp64(eG);
-  const float ehf = float(e1), ehif = float(e1i);
-  const float m2vl = float(-2.0 * v2);
-  const float eqf = ex2_approx(m2vl * hf);
-  const float a1 = -expm1f(-2.0f * vf * hf);
-  // two-node steps of the packed recurrences
-  const float eq2f = eqf * eqf, eh2f = float(e2), ehi2f = float(e1i * e1i), h2f = 2.0f * hf;
-  const float a2 = -expm1f(-4.0f * vf * hf);            // p_{m+2} = p_m + q_m (1 - e^{-4vh})
-  const double tb = fma((double)mb, h, t0);
-  const double ebx = exp(tb);
-  double XpG = hx2 * ebx, XmG = hx2 * rcp64(ebx);
-  // The FP32 cosh state is kept scaled by 2^-sig so that e^t stays below 2^64
-  // up to t1, leaving room for weights up to ~2^30 in the FP32 sums (e^t
-  // overflows FP32 beyond t = 88.7, where |d log K/dx| ~ cosh t_p itself
-  // approaches FLT_MAX); sig = 0 whenever t1 < 44, i.e. on every config.
-  const int sig = max(0, (int)ceil(fma((double)n, h, t0) * kLog2e) - 64);
-  const double sc_sig = ldexp(1.0, sig);
-  const double sc_et = ldexp(0.5 / hx2, -sig);
-  const float k_eti = float(ldexp(0.25, -2 * sig));
-  double S0 = 0.0, S1 = 0.0, S2 = 0.0;
-  double md = (double)mb;
-  int m = mb;
-#pragma unroll 1
-  while (m < me) {
-    const int c1 = min(m + CH, me);
-    const double tcd = fma(md, h, t0);
-    const float tcf = float(tcd);
-    // FP32 state re-anchored per block: e^{+-t}/2, q = e^{-2vt}, p = 1 - q
-    float etf = float(XpG * sc_et);                      // 2^-sig e^{+-t} / 2 (FP32 state)
-    float etif = k_eti * rcp_approx(etf);
-    float q = ex2_approx(m2vl * tcf);
-    float p = -expm1f(-2.0f * vf * tcf);
-    float tf = tcf;
-    float B0 = 0.0f, B1 = 0.0f, B2 = 0.0f;
-    // The FP32 state of node pairs (j, j+1) in f32x2 registers: one FFMA2 /
-    // FMUL2 / FADD2 serves two nodes, and the accumulating FFMA2s read three
-    // register pairs in 3 cycles instead of two 3-register FFMAs in 4.
-    float2 q2 = f2(q, q * eqf), p2 = f2(p, fmaf(q, a1, p));
-    float2 et2 = f2(etf, etf * ehf), eti2 = f2(etif, etif * ehif), t2 = f2(tf, tf + hf);
-    float2 C0 = f2s(0.0f), C1 = f2s(0.0f), C2 = f2s(0.0f);
-#pragma unroll 1
-    for (; m + G <= c1; m += G) {
-      const double tc = fma(md, h, t0);
-      md += (double)G;
-      const double Bc = fma(v2, tc, cst);
-      float E[G];
-      double xp = XpG, xm = XmG;
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const double X = xp + xm;
-        const double A = (j == 0 ? Bc : fma(double(j), v2h, Bc)) - X;
-        E[j] = exp2_fixed(A);
-        if (j + 1 < G) { xp *= e1; xm *= e1i; }
-      }
-      XpG *= eG; XmG *= eGi;
-#pragma unroll
-      for (int j = 0; j < G; j += 2) {
-        const float2 Ej = f2(E[j], E[j + 1]);
-        const float2 w = fma2(Ej, q2, Ej);                // E (1 + q)
-        C0 = add2(C0, w);
-        // (cosh t from X by F2F.F32.F64 per node measured 6% slower: XU-bound)
-        if (DX) C2 = fma2(w, add2(et2, eti2), C2);
-        if (DV) C1 = fma2(mul2(Ej, t2), p2, C1);
-        if (DV) p2 = fma2(q2, f2s(a2), p2);
-        q2 = mul2(q2, f2s(eq2f));
-        et2 = mul2(et2, f2s(eh2f));
-        eti2 = mul2(eti2, f2s(ehi2f));
-        t2 = add2(t2, f2s(h2f));
-      }
-    }
-    B0 = C0.x + C0.y; B1 = C1.x + C1.y; B2 = C2.x + C2.y;
-    q = q2.x; p = p2.x; etf = et2.x; etif = eti2.x; tf = t2.x;
-#pragma unroll 1
-    for (; m < c1; ++m) {                                // remainder, one node at a time
-      const double t = fma(md, h, t0);
-      md += 1.0;
-      const float E = exp2_fixed(fma(v2, t, cst) - (XpG + XmG));
-      XpG *= e1; XmG *= e1i;
-      const float w = fmaf(E, q, E);
-      B0 += w;
-      if (DX) B2 = fmaf(w, etf + etif, B2);
-      if (DV) B1 = fmaf(E * tf, p, B1);
-      if (DV) p = fmaf(q, a1, p);
-      q *= eqf;
-      etf *= ehf;
-      etif *= ehif;
-      tf += hf;
-    }
-    S0 += B0; S1 += B1; S2 += double(B2) * sc_sig;
-  }
-  // half weights of nodes 0 and n, evaluated directly; X at
-  // node 0 is the exact start state (mb == 0) and at node n = me - 1 one
-  // step back from the final recurrence state
-  auto half_node = [&](int mm, double X) {
-    const double t = fma((double)mm, h, t0);
-    const float E = 0.5f * exp2_fixed(fma(v2, t, cst) - X);
-    const float tf1 = float(t);
-    const float q1 = ex2_approx(m2vl * tf1);
-    const float w = fmaf(E, q1, E);
-    S0 -= w;
-    if (DX) S2 -= double(w) * (X * (1.0 / (2.0 * hx2)));
-    if (DV) S1 -= double(E * tf1) * (-expm1f(-2.0f * vf * tf1));
-  };
-  if (mb == 0) half_node(0, hx2 * (ebx + rcp64(ebx)));
-  if (mb < me && me == n + 1) half_node(n, fma(XpG, e1i, XmG * e1));
-  return Sums32{S0, S1, S2};
-}
 
-// FP32 entry point, group-base form (v3).  The FP64 fixed-point exponent of
-// quad_f32_v2 is formed once per group of 4 nodes, at the group's first node
+// FP32 entry point, group-base form (v3).  The FP64 fixed-point exponent
+// (exp2_fixed above; round 1 formed it at every node) is formed once per group
+// of 4 nodes, at the group's first node
 // c: A_c = v2 t_c - X_c + cst (X = x cosh t log2(e) = Xp + Xm, Xp/m =
 // (x log2(e)/2) e^{+-t}; 7 FP64 operations), E_c = 2^{a2_c} by exp2_fixed.
 // The other nodes j = 1..3 of the group differ from it by an exponent that
