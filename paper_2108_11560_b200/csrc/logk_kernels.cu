@@ -162,8 +162,7 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   // hide their latency (it stalled every warp at its first use of x).
   const double vraw = live ? vin[i] : 1.0;
   const double x = live ? xin[i] : 1.0;
-  load_exp_table();
-  __syncthreads();
+  load_exp_table_sync();
   f64_element<LOGK, DV, DX, LPE>(vraw, x, live, sub, i, logk, dlogk_dv, dlogk_dx, nbins,
                                  range_mode);
 }
@@ -184,8 +183,7 @@ logk_f64_hess_kernel(const double *__restrict__ vin, const double *__restrict__ 
   const bool live = i < n_el;
   const double vraw = live ? vin[i] : 1.0;   // loads issued ahead of the table copy
   const double x = live ? xin[i] : 1.0;
-  load_exp_table();
-  __syncthreads();
+  load_exp_table_sync();
   const bool valid = valid_input(vraw, x);
   const double v = fabs(vraw);
   const long long vbits = __double_as_longlong(vraw);
@@ -226,8 +224,7 @@ logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ 
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const double vraw = i < n_el ? vin[i] : 1.0;
   const double x = i < n_el ? xin[i] : 1.0;
-  load_exp_table();
-  __syncthreads();
+  load_exp_table_sync();
   if (i >= n_el) return;
   const bool valid = valid_input(vraw, x);
   double t0 = 0.0, t1 = 0.0, gp = 0.0, dmin = 0.0, tp = 0.0;

@@ -40,8 +40,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
                double g, int nbins, double *__restrict__ partial) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const double yi = i < n ? y[i] : 0.0;   // issued ahead of the table copy
-  load_exp_table();
-  __syncthreads();
+  load_exp_table_sync();
   __shared__ double red[kNigOut][kNigThreads / 32];
   double c[kNigOut] = {0.0, 0.0, 0.0, 0.0, 0.0};
   if (i < n) {

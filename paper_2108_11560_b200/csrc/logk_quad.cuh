@@ -72,11 +72,43 @@ __device__ __align__(16) const unsigned long long kExp2TablePc[kExpTab] = {
 // immediate/uniform base (no per-node base-register add).
 __shared__ __align__(16) double g_exp_tab[kExpTab];
 
-// Block-cooperative copy of the table to shared memory (caller syncs).
-__device__ __forceinline__ void load_exp_table() {
+#ifndef BLK_TMA_TABLE
+#define BLK_TMA_TABLE 1
+#endif
+// The table copy to shared memory, complete and visible to the whole block on
+// return.  BLK_TMA_TABLE: one bulk asynchronous copy (TMA engine,
+// cp.async.bulk global -> shared, 16 KB) issued by thread 0 and signalled
+// through an mbarrier transaction count, instead of every thread moving its
+// share through registers (8 LDG.128 + 8 STS.128 per thread of a 128-thread
+// block).
+__shared__ __align__(8) unsigned long long g_tab_bar;
+__device__ __forceinline__ void load_exp_table_sync() {
+#if BLK_TMA_TABLE
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&g_tab_bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(g_exp_tab);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((unsigned)sizeof(g_exp_tab)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(kExp2TablePc), "r"((unsigned)sizeof(g_exp_tab)), "r"(bar)
+                 : "memory");
+  }
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar) : "memory");
+#else
   const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(kExp2TablePc);
   ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(g_exp_tab);
   for (int j = threadIdx.x; j < kExpTab / 2; j += blockDim.x) dst[j] = src[j];
+  __syncthreads();
+#endif
 }
 
 // 2^(k/2048) for k in [-2^21, 2^21): one LDS.64 and one IMAD.

@@ -21,8 +21,7 @@ __global__ void __launch_bounds__(128)
 plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 PlanRec *__restrict__ plans, int nbins, int range_mode) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  load_exp_table();   // for make_plan_f64_tab, before any thread leaves
-  __syncthreads();
+  load_exp_table_sync();   // for make_plan_f64_tab, before any thread leaves
   if (i >= n_el) return;
   const double vraw = vin[i], x = xin[i];
   const bool valid = (x > 0.0) && isfinite(x) && isfinite(vraw);
@@ -51,8 +50,7 @@ __global__ void __launch_bounds__(128, BLK_MINB)
 quad_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 const PlanRec *__restrict__ plans, double *__restrict__ logk,
                 double *__restrict__ dlogk_dv, double *__restrict__ dlogk_dx, int nbins) {
-  load_exp_table();
-  __syncthreads();
+  load_exp_table_sync();
   const double *tab = g_exp_tab;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_el) return;
