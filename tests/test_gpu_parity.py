@@ -228,7 +228,7 @@ def test_extreme_domain(kernel):
     value, and test_oracle_pins.py::test_large_x_dv_vs_brute_force pins it
     within 0.5 kappa of the long-double brute force -- so the derivative
     tolerance here is max(1e-10, 5 kappa).  Measured against the oracle: <= 0.05
-    kappa here, <= 1.96 kappa on the wide-domain fuzz (profiles/r02x_kappa.log)."""
+    kappa here, <= 1.96 kappa on the wide-domain fuzz (profiles/r02zh_kappa.log)."""
     v = np.array([0, 0, 5, 0, 10, 2000, 5000, 1e4, 0.5, 5, 0, 30.0, 2e4, 3.0])
     x = np.array([1e3, 1e4, 1e5, 1e6, 1e8, 1e-3, 1e-4, 1e-2, 1e-6, 1e-10, 1e-8, 1e-30, 1.0, 1e-40])
     got = run_gpu(v, x, kernel=kernel)
@@ -758,5 +758,40 @@ def test_large_order_cancellation(lanes):
     e0 = errors(got["logk"], lk, "logk")
     assert np.all(e0 <= 2.5 * tol_l), ((e0 / tol_l).max(), v[np.argmax(e0 / tol_l)])
     tol_d = np.maximum(1e-10, 5 * kappa)
+    assert np.all(errors(got["dv"], dv, "dv") <= tol_d)
+    assert np.all(errors(got["dx"], dx, "dx") <= tol_d)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_regime_boundary_fuzz(seed):
+    """Orders next to the regime boundary v^2 = x, where the peak
+    t_p -> 0, g''(t_p) -> 0 and the range brackets built from the curvature
+    (R5b) degenerate and must fall back to Alg. 1: v = sqrt(x) (1 +- delta),
+    delta in logU[1e-8, 0.3], x in logU[1e-6, 1e4]; FP64 and FP32 entry points
+    at the north_star tolerances."""
+    rng = np.random.default_rng(300 + seed)
+    n = 8000
+    x = 10.0 ** rng.uniform(-6, 4, n)
+    delta = 10.0 ** rng.uniform(-8, np.log10(0.3), n) * np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    v = np.sqrt(x) * (1.0 + delta)
+    got = run_gpu(v, x)
+    assert_parity(got, run_oracle(v, x), "f64", "regime boundary")
+    v32, x32 = v.astype(np.float32), x.astype(np.float32)
+    got32 = run_gpu(v32, x32)
+    assert_parity(got32, run_oracle(v32, x32), "f32", "regime boundary f32")
+
+
+def test_peak_bracket_extremes():
+    """The analytic peak bracket asinh(v/x) (R5b) at its extremes: v/x up to
+    1e34 (the FP32 range finder's domain edge x = 1e-30, v = 1e4) and down to
+    v/x ~ 1/v (v^2 just above x), against the oracle."""
+    v = np.array([1e4, 1e4, 5e3, 1.0, 1e-3, 0.5, 30.0, 99.0, 1e4, 2.0])
+    x = np.array([1e-30, 1e-20, 1e-10, 0.999, 0.99e-6, 0.2499, 1e-30, 9800.0, 9.9e3, 3.99])
+    got = run_gpu(v, x)
+    lk, dv, dx, plan = oracle.logk(v, x, NB, with_plan=True)
+    from parity import errors
+    kappa = np.finfo(float).eps * (x + v * plan[:, 0] + 40.0)   # tolerance note, DESIGN §3
+    tol_d = np.maximum(1e-10, 5 * kappa)
+    assert np.all(errors(got["logk"], lk, "logk") <= 1e-12)
     assert np.all(errors(got["dv"], dv, "dv") <= tol_d)
     assert np.all(errors(got["dx"], dx, "dx") <= tol_d)
