@@ -3,19 +3,23 @@
 // Alg. 1 FindRange, Alg. 2 FindZero and lines 2-9 of Alg. 3 (PAPER.md
 // P:144-218), with the readings recorded in DESIGN.md §3
 // (R1 orientation F(a) < 0 <= F(b), return a; R3 clip to [a, mid];
-// R4 fixed 10 iterations; R5 lo = t_s when m = 0; R18 Newton with F'(a)=0
-// -> bisection point).  Independent of oracle/ (no shared code).
+// R4 at most 10 iterations, the "until" clause on working tolerances;
+// R5 lo = t_s when m = 0; R5b brackets from the shape of g in the FP32
+// finder; R18 Newton with F'(a)=0 -> bisection point).  Independent of
+// oracle/ (no shared code).
 //
-// Two implementations of the same algorithm:
+// Two implementations:
 //   * PlanF32: FP32 FMA pipe + MUFU (ex2/lg2/rcp.approx).  The two point
 //     evaluations of one FindZero iteration (at the bisection point and at the
 //     Newton point) are independent, so they run as packed f32x2 operations
 //     (FFMA2/FADD2/FMUL2, sm_100) -- half the issue slots.  The plan only has
 //     to be conservative at the log-eps level (R20), so finding it
-//     in FP32 leaves the FP64 pipe to the quadrature.
-//   * PlanF64: libdevice double functions -- the paper's working-precision
-//     variant; used outside the FP32-safe domain and on request
-//     (BLK_RANGE_F64).
+//     in FP32 leaves the FP64 pipe to the quadrature.  Used from 64 bins (the
+//     FP32 entry point: from 16) inside its safe domain.
+//   * PlanF64 / PlanF64Tab: double -- the paper's working-precision variant
+//     with Alg. 1 as printed, stopping only once converged (the oracle's
+//     ranges); used for coarse grids, outside the FP32-safe domain and on
+//     request (BLK_RANGE_F64).
 // Every point evaluation returns F and F' jointly (they share e^t, e^-t and
 // q = e^{-2vt}).
 #pragma once
