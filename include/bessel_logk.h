@@ -92,14 +92,23 @@ typedef struct {
     int block_threads;
     /* Kernel variant: BLK_KERNEL_AUTO or BLK_KERNEL_SIMPLE (the same
      * kernel: one element -- or lanes_per_element lanes -- per thread, both
-     * phases in every warp).  Any other value is BLK_EINVAL.  (A
-     * warp-specialised producer/consumer variant was measured 10-20% slower
-     * and removed.) */
+     * phases in every warp), or BLK_KERNEL_VEC128 (below).  Any other value
+     * is BLK_EINVAL.  (A warp-specialised producer/consumer variant was
+     * measured 10-20% slower and removed.) */
     int kernel;
 } blk_options;
 
 #define BLK_KERNEL_AUTO 0
 #define BLK_KERNEL_SIMPLE 1
+/* One element per thread with warp-cooperative 128-bit loads and stores of
+ * the v / x / output streams (BASELINE.json north_star (3)): each warp moves
+ * its 32 elements as 16-byte vectors and transposes them through shared
+ * memory.  lanes_per_element must be 0 or 1 (else BLK_EINVAL).  Needs every
+ * non-NULL stream 16-byte aligned; otherwise the scalar-I/O kernel runs.
+ * Results are bit-identical to BLK_KERNEL_SIMPLE with one lane per element.
+ * Not the default: measured 0.8% (FP64) / 1.7% (FP32) slower on B200, the
+ * kernels being compute-bound at ~3% of HBM bandwidth. */
+#define BLK_KERNEL_VEC128 2
 
 /*
  * FP64 entry point.  eps = 2^-52 (log eps = -36.0437, R9).

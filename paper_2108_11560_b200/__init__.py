@@ -20,7 +20,7 @@ import re
 
 __all__ = [
     "BLK_OK", "BLK_EINVAL", "BLK_ECUDA", "BLK_RANGE_AUTO", "BLK_RANGE_F64",
-    "BLK_KERNEL_AUTO", "BLK_KERNEL_SIMPLE",
+    "BLK_KERNEL_AUTO", "BLK_KERNEL_SIMPLE", "BLK_KERNEL_VEC128",
     "BesselLogKError", "lib", "library_path", "header_functions",
     "bessel_logk_f64", "bessel_logk_f32", "log_bessel_k", "bessel_logk_f64_host",
     "bessel_logk_f32_host",
@@ -35,7 +35,7 @@ HEADER = os.path.join(_ROOT, "include", "bessel_logk.h")
 
 BLK_OK, BLK_EINVAL, BLK_ECUDA = 0, 1, 2
 BLK_RANGE_AUTO, BLK_RANGE_F64 = 0, 1
-BLK_KERNEL_AUTO, BLK_KERNEL_SIMPLE = 0, 1
+BLK_KERNEL_AUTO, BLK_KERNEL_SIMPLE, BLK_KERNEL_VEC128 = 0, 1, 2
 BLK_MB_UNROLL = 16
 # Trapezoid intervals used when the caller gives none (the paper states no n,
 # P:222; R10).

@@ -20,6 +20,7 @@
 #include "logk_quad.cuh"
 #include "logk_range.cuh"
 #include "logk_nig.cuh"
+#include "logk_io.cuh"
 #ifdef BLK_DIAG
 #include "logk_split.cuh"   // diagnostics build only (tools/): the two phases as two kernels
 #endif
@@ -99,13 +100,11 @@ __device__ __forceinline__ bool element_plan_f64(double v, double x, int nbins, 
 }
 
 // One element (or one lane of LPE) of the FP64 path after the exp table is
-// in shared memory: a1-a7 for (vraw, x), outputs stored by lane sub == 0.
+// in shared memory: a1-a7 for (vraw, x); the caller stores the outputs.
 template <bool LOGK, bool DV, bool DX, int LPE>
-__device__ __forceinline__ void f64_element(double vraw, double x, bool live, int sub, size_t i,
-                                            double *__restrict__ logk,
-                                            double *__restrict__ dlogk_dv,
-                                            double *__restrict__ dlogk_dx, int nbins,
-                                            int range_mode) {
+__device__ __forceinline__ void f64_element(double vraw, double x, int sub, int nbins,
+                                            int range_mode, double &o_logk, double &o_dv,
+                                            double &o_dx) {
   const double *tab = g_exp_tab;
   const bool valid = valid_input(vraw, x);
   const double v = fabs(vraw);
@@ -133,25 +132,28 @@ __device__ __forceinline__ void f64_element(double vraw, double x, bool live, in
     if (DX) s.S2 = group_sum<LPE>(s.S2);
   }
   BLK_TL(2);
-  if (!live || sub != 0) return;
   // a7: epilogue
   const double nanv = __longlong_as_double(0x7ff8000000000000ULL);
   const double r = rcp64(s.S0);
-  if (LOGK) logk[i] = ok ? gp + log_sum(h * s.S0) : nanv;
-  if (DV) dlogk_dv[i] = ok ? sgn * (s.S1 * r) : nanv;
-  if (DX) dlogk_dx[i] = ok ? -(s.S2 * r) : nanv;
+  if (LOGK) o_logk = ok ? gp + log_sum(h * s.S0) : nanv;
+  if (DV) o_dv = ok ? sgn * (s.S1 * r) : nanv;
+  if (DX) o_dx = ok ? -(s.S2 * r) : nanv;
 }
 
 // The FP64 kernel: one element per lane (or LPE lanes per element).  (Two to
 // eight elements per thread in sequence, amortising the table copy and the
 // block launch, measured 2-6% slower on c2/c3/c5: the block-by-block launch
 // staggers the XU-bound plan and the FP64-bound quadrature across warps,
-// profiles/r02j_ept.log.)
-template <bool LOGK, bool DV, bool DX, int LPE>
+// profiles/r02j_ept.log.)  VEC (one element per lane only; the host selects it
+// for BLK_KERNEL_VEC128 when every stream is 16-B aligned): 128-bit
+// warp-cooperative loads and stores (logk_io.cuh) for warps of 32 in-range
+// elements, the scalar path for the ragged last warp.
+template <bool LOGK, bool DV, bool DX, int LPE, bool VEC = false>
 __global__ void __launch_bounds__(128, BLK_MINB)
 logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, size_t n_el,
                 double *__restrict__ logk, double *__restrict__ dlogk_dv,
                 double *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  static_assert(!VEC || LPE == 1, "128-bit I/O needs one element per lane");
   BLK_TL(0);
   const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t i = gtid / LPE;
@@ -160,11 +162,36 @@ logk_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
   // Lanes past the end still take part in the shuffles (full-warp masks).
   // The input loads are issued before the table copy and its barrier, which
   // hide their latency (it stalled every warp at its first use of x).
-  const double vraw = live ? vin[i] : 1.0;
-  const double x = live ? xin[i] : 1.0;
-  load_exp_table_sync();
-  f64_element<LOGK, DV, DX, LPE>(vraw, x, live, sub, i, logk, dlogk_dv, dlogk_dx, nbins,
-                                 range_mode);
+  double vraw = 1.0, x = 1.0;
+  if constexpr (VEC) {
+    __shared__ __align__(16) double s_io[kIoWarps * kIoPerWarp];
+    const bool full = (gtid | 31) < n_el;   // warp-uniform
+    // transposed before the table barrier: finishing it after the barrier
+    // perturbs ptxas's node-loop schedule (-3.6% on c3, profiles/r02io_vec128_ab.log)
+    if (full) io_load_finish(s_io, io_load_issue(vin, xin, i), i, vraw, x);
+    else if (live) { vraw = vin[i]; x = xin[i]; }
+    load_exp_table_sync();
+    double o0, o1, o2;
+    f64_element<LOGK, DV, DX, 1>(vraw, x, 0, nbins, range_mode, o0, o1, o2);
+    if (full) {
+      // the barrier separates the input reads of s_io from these writes
+      io_store<double, LOGK, DV, DX, false>(s_io, i, o0, o1, o2, logk, dlogk_dv, dlogk_dx);
+    } else if (live) {
+      if (LOGK) logk[i] = o0;
+      if (DV) dlogk_dv[i] = o1;
+      if (DX) dlogk_dx[i] = o2;
+    }
+  } else {
+    if (live) { vraw = vin[i]; x = xin[i]; }
+    load_exp_table_sync();
+    double o0, o1, o2;
+    f64_element<LOGK, DV, DX, LPE>(vraw, x, sub, nbins, range_mode, o0, o1, o2);
+    if (live && sub == 0) {
+      if (LOGK) logk[i] = o0;
+      if (DV) dlogk_dv[i] = o1;
+      if (DX) dlogk_dx[i] = o2;
+    }
+  }
 }
 
 // Second derivatives in the same pass: the three
@@ -242,11 +269,9 @@ logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ 
 #define BLK_F32_MINB 5
 #endif
 template <bool LOGK, bool DV, bool DX, int LPE>
-__device__ __forceinline__ void f32_element(float vraw, float x, bool live, int sub, size_t i,
-                                            float *__restrict__ logk,
-                                            float *__restrict__ dlogk_dv,
-                                            float *__restrict__ dlogk_dx, int nbins,
-                                            int range_mode) {
+__device__ __forceinline__ void f32_element(float vraw, float x, int sub, int nbins,
+                                            int range_mode, float &o_logk, float &o_dv,
+                                            float &o_dx) {
   const bool valid = (x > 0.0f) && isfinite(x) && isfinite(vraw);
   const float v = fabsf(vraw);
   const float sgn = (vraw < 0.0f) ? -1.0f : 1.0f;
@@ -282,27 +307,48 @@ __device__ __forceinline__ void f32_element(float vraw, float x, bool live, int 
     if (DV) s.S1 = group_sum<LPE>(s.S1);
     if (DX) s.S2 = group_sum<LPE>(s.S2);
   }
-  if (!live || sub != 0) return;
   const float nanv = __int_as_float(0x7fc00000);
   const double r0 = rcp64(s.S0);
-  if (LOGK) logk[i] = ok ? gp + logf(float(double(h) * s.S0)) : nanv;
-  if (DV) dlogk_dv[i] = ok ? sgn * float(s.S1 * r0) : nanv;
-  if (DX) dlogk_dx[i] = ok ? -float(s.S2 * r0) : nanv;
+  if (LOGK) o_logk = ok ? gp + logf(float(double(h) * s.S0)) : nanv;
+  if (DV) o_dv = ok ? sgn * float(s.S1 * r0) : nanv;
+  if (DX) o_dx = ok ? -float(s.S2 * r0) : nanv;
 }
 
-template <bool LOGK, bool DV, bool DX, int LPE>
+template <bool LOGK, bool DV, bool DX, int LPE, bool VEC = false>
 __global__ void __launch_bounds__(128, BLK_F32_MINB)
 logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, size_t n_el,
                 float *__restrict__ logk, float *__restrict__ dlogk_dv,
                 float *__restrict__ dlogk_dx, int nbins, int range_mode) {
+  static_assert(!VEC || LPE == 1, "128-bit I/O needs one element per lane");
   const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t i = gtid / LPE;
   const int sub = (int)(gtid % LPE);
   const bool live = i < n_el;
-  const float vraw = live ? vin[i] : 1.0f;
-  const float x = live ? xin[i] : 1.0f;
-  f32_element<LOGK, DV, DX, LPE>(vraw, x, live, sub, i, logk, dlogk_dv, dlogk_dx, nbins,
-                                 range_mode);
+  float vraw = 1.0f, x = 1.0f;
+  if constexpr (VEC) {
+    __shared__ __align__(16) float s_io[kIoWarps * kIoPerWarp];
+    const bool full = (gtid | 31) < n_el;   // warp-uniform
+    if (full) io_load_finish(s_io, io_load_issue(vin, xin, i), i, vraw, x);
+    else if (live) { vraw = vin[i]; x = xin[i]; }
+    float o0, o1, o2;
+    f32_element<LOGK, DV, DX, 1>(vraw, x, 0, nbins, range_mode, o0, o1, o2);
+    if (full) {
+      io_store<float, LOGK, DV, DX>(s_io, i, o0, o1, o2, logk, dlogk_dv, dlogk_dx);
+    } else if (live) {
+      if (LOGK) logk[i] = o0;
+      if (DV) dlogk_dv[i] = o1;
+      if (DX) dlogk_dx[i] = o2;
+    }
+  } else {
+    if (live) { vraw = vin[i]; x = xin[i]; }
+    float o0, o1, o2;
+    f32_element<LOGK, DV, DX, LPE>(vraw, x, sub, nbins, range_mode, o0, o1, o2);
+    if (live && sub == 0) {
+      if (LOGK) logk[i] = o0;
+      if (DV) dlogk_dv[i] = o1;
+      if (DX) dlogk_dx[i] = o2;
+    }
+  }
 }
 
 // ------------------------------------------------------------ microbenchmarks
@@ -401,7 +447,10 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
     kernel = opts->kernel;
     if (opts->block_threads) threads = opts->block_threads;
   }
-  if (kernel != BLK_KERNEL_AUTO && kernel != BLK_KERNEL_SIMPLE) return fail(BLK_EINVAL, "bad kernel variant");
+  if (kernel != BLK_KERNEL_AUTO && kernel != BLK_KERNEL_SIMPLE && kernel != BLK_KERNEL_VEC128)
+    return fail(BLK_EINVAL, "bad kernel variant");
+  if (kernel == BLK_KERNEL_VEC128 && lanes > 1)
+    return fail(BLK_EINVAL, "BLK_KERNEL_VEC128 needs lanes_per_element 0 or 1");
   if (nbins < 2 || nbins > BLK_MAX_NBINS) return fail(BLK_EINVAL, "nbins out of range [2, 65536]");
   if (n > 0 && !o1 && !o2 && !o3) return fail(BLK_EINVAL, "all outputs are NULL");
   if (n > 0 && (!v || !x)) return fail(BLK_EINVAL, "v or x is NULL");
@@ -409,6 +458,12 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
   if (lanes < 0 || lanes > 32 || (lanes & (lanes - 1))) return fail(BLK_EINVAL, "lanes_per_element must be 0 or a power of two <= 32");
   if (threads < 32 || threads > 128 || threads % 32) return fail(BLK_EINVAL, "block_threads must be a multiple of 32 in [32, 128]");
   if (n > ((size_t)1 << 40)) return fail(BLK_EINVAL, "n too large");
+  if (kernel == BLK_KERNEL_VEC128) {
+    lanes = 1;
+    const uintptr_t m = (uintptr_t)v | (uintptr_t)x | (uintptr_t)o1 | (uintptr_t)o2 | (uintptr_t)o3;
+    if (m & 15u) kernel = BLK_KERNEL_SIMPLE;   // scalar I/O, identical results
+    return BLK_OK;
+  }
   kernel = BLK_KERNEL_SIMPLE;
   if (lanes == 0) lanes = auto_lanes(n, nbins);
   return BLK_OK;
@@ -435,9 +490,11 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
 #ifdef BLK_MIN_INSTANCES
 // tuning-variant builds (tools/build_variants.py): one element per lane only
 #define BLK_DISPATCH_LPE(KER, L, O1, O2, O3) \
+  if (vec) return launch_k(KER<O1, O2, O3, 1, true>, n, 1, th, stream, v, x, a, b, c, nbins, mode); \
   return launch_k(KER<O1, O2, O3, 1>, n, 1, th, stream, v, x, a, b, c, nbins, mode);
 #else
 #define BLK_DISPATCH_LPE(KER, L, O1, O2, O3)                                        \
+  if (vec) return launch_k(KER<O1, O2, O3, 1, true>, n, 1, th, stream, v, x, a, b, c, nbins, mode); \
   switch (L) {                                                                      \
     case 1: return launch_k(KER<O1, O2, O3, 1>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
     case 2: return launch_k(KER<O1, O2, O3, 2>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
@@ -455,6 +512,7 @@ blk_status run(const T *v, const T *x, size_t n, T *a, T *b, T *c, int nbins,
   blk_status st = validate(v, x, n, a, b, c, nbins, opts, lanes, mode, th, kernel);
   if (st != BLK_OK) return st;
   if (n == 0) return BLK_OK;
+  const bool vec = kernel == BLK_KERNEL_VEC128;
   const int sel = (a ? 4 : 0) | (b ? 2 : 0) | (c ? 1 : 0);
   if constexpr (sizeof(T) == 8) {
     switch (sel) {

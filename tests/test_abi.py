@@ -66,7 +66,8 @@ def test_invalid_arguments(L):
     assert b"nbins" in L.bessel_logk_last_error() or L.bessel_logk_last_error()
     bad = [blk._Options(3, 0, 0), blk._Options(64, 0, 0), blk._Options(0, 2, 0),
            blk._Options(0, 0, 48), blk._Options(0, 0, 256), blk._Options(-1, 0, 0),
-           blk._Options(0, 0, 0, 2), blk._Options(0, 0, 0, -1)]
+           blk._Options(0, 0, 0, 3), blk._Options(0, 0, 0, -1),
+           blk._Options(2, 0, 0, blk.BLK_KERNEL_VEC128)]   # 128-bit I/O: one lane per element
     for o in bad:
         assert _f64(L, FAKE, FAKE, 10, FAKE, None, None, 128, o) == blk.BLK_EINVAL
     assert L.bessel_logk_f32(FAKE, FAKE, 10, None, None, None, 128, None) == blk.BLK_EINVAL
