@@ -436,6 +436,9 @@ def main():
                                "frac": iss / fp64_ops if iss else None,
                                "inst_per_element": counts["fp64_inst_per_element"] if counts else None},
                 "flops_per_element": counts["fp64_flops_per_element"] if counts else None,
+                "fp32_frac": (counts["fp32_flops_per_element"] * rate / 1e12) / (fp32_ops * 2 / 1e12)
+                if counts else None,
+                "mufu_frac": counts["mufu_per_element"] * rate / mufu_ops if counts else None,
                 "peak_source": "in-run DFMA microbenchmark (blk_microbench_fp64; 2 flops per DFMA); "
                                f"nominal {NOMINAL_FP64_TFLOPS:.1f} TF/s = 148 SM x 64 DFMA/clk x 1.965 GHz"}
     else:
