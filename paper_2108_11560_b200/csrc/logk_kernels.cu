@@ -291,7 +291,7 @@ __device__ __forceinline__ void f32_element(float vraw, float x, int sub, int nb
     ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
   }
   Sums32 s{0.0, 0.0, 0.0};
-  const float h = (t1 - t0) / nbins;
+  const float h = (t1 - t0) * rcp_approx((float)nbins);   // the grid need not be IEEE-exact
   if (ok) {
     int mb, me;
     lane_bins<LPE>(nbins, sub, mb, me);

@@ -49,6 +49,23 @@ __device__ __forceinline__ float rcp_approx(float a) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a));
   return y;
 }
+__device__ __forceinline__ float sqrt_approx(float a) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(a));
+  return y;
+}
+#ifndef BLK_SMART_FAST
+#define BLK_SMART_FAST 1
+#endif
+// Quotients and square roots of the R5b bracket guesses: every guess is
+// checked by evaluating F there, so MUFU approximations (2 instructions)
+// serve instead of IEEE division / sqrt (~10 with the FCHK slow-path branch).
+__device__ __forceinline__ float guess_div(float a, float b) {
+  return BLK_SMART_FAST ? a * rcp_approx(b) : a / b;
+}
+__device__ __forceinline__ float guess_sqrt(float a) {
+  return BLK_SMART_FAST ? sqrt_approx(a) : sqrtf(a);
+}
 
 // ------------------------------------------------------------ packed helpers
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -279,9 +296,9 @@ __device__ __forceinline__ bool smart_peak_bracket(const PlanF32 &P, const PFN &
   // FP32 resolution.  [0, t*] brackets it (g'(0) = 0).  (t* is moved out by
   // 2^-10 relative + 1e-4: where v t* >> 1, g'(t*) is below the FP32
   // rounding of its two ~v-sized terms and could test >= 0.)
-  const float z = P.v / P.x;
+  const float z = guess_div(P.v, P.x);
   const float ta = z > 1e4f ? lg2_approx(2.0f * z) * PlanF32::kLn2f
-                            : lg2_approx(z + sqrtf(fmaf(z, z, 1.0f))) * PlanF32::kLn2f;
+                            : lg2_approx(z + guess_sqrt(fmaf(z, z, 1.0f))) * PlanF32::kLn2f;
   const float ts = fmaf(ta, 1.0009765625f, 1e-4f);
   pf(ts, Fh, dFh);
   if (!(Fh < 0.0f && isfinite(dFh))) return false;
@@ -301,7 +318,7 @@ __device__ __forceinline__ void smart_t0_bracket(const DFN &df, float tp, float 
   df(tq, Fq, dFq);
   if (Fq < 0.0f) { a = tq; Fa = Fq; dFa = dFq; }
   else if (dFq > 0.0f) {
-    const float tz = fmaxf(tq - Fq / dFq, 0.0f);
+    const float tz = fmaxf(tq - guess_div(Fq, dFq), 0.0f);
     float Fz, dFz;
     df(tz, Fz, dFz);
     if (Fz < 0.0f) { a = tz; Fa = Fz; dFa = dFz; b = tq; }
@@ -316,7 +333,7 @@ __device__ __forceinline__ bool smart_t1_bracket(const DFN &df, float tp, float 
   df(tq, Fh, dFh);
   if (Fh < 0.0f) { hi = tq; lo = tp; return true; }
   if (dFh < 0.0f) {
-    const float tz = tq - Fh / dFh;
+    const float tz = tq - guess_div(Fh, dFh);
     float Fz, dFz;
     df(tz, Fz, dFz);
     if (Fz < 0.0f && isfinite(dFz)) { hi = tz; lo = tq; Fh = Fz; dFh = dFz; return true; }
@@ -326,7 +343,7 @@ __device__ __forceinline__ bool smart_t1_bracket(const DFN &df, float tp, float 
 // half-width of the quadratic model g ~ g_p - K (t - t_p)^2 / 2 at the eps
 // level, when usable for the brackets (< 32 keeps every probe in FP32 range)
 __device__ __forceinline__ float model_halfwidth(float L, float K) {
-  const float dq = sqrtf(-2.0f * L / K);
+  const float dq = guess_sqrt(guess_div(-2.0f * L, K));
   return (isfinite(dq) && dq > 0.0f && dq < 32.0f) ? dq : 0.0f;
 }
 
