@@ -475,10 +475,18 @@ __device__ __forceinline__ void v2_accumulate(double E, double q, double X, doub
   }
 }
 
+#ifndef BLK_HALF_IN_REM
+#define BLK_HALF_IN_REM 1
+#endif
+// half_last: node ie - 1 is node n (this lane owns it); when it falls in the
+// remainder loop (the node count is not a multiple of G, e.g. n = 128) it is
+// taken there with its trapezoid weight 1/2 and the function returns
+// true -- no separate end-node correction needed.
 template <bool DV, bool DX, bool HESS = false>
-__device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, double h,
-                                              double s_mid, int ib, int ie, Sums64 &out) {
-  if (ie <= ib) return;
+__device__ __forceinline__ bool nodes_fp64_v2(double v, double x, double t0, double h,
+                                              double s_mid, int ib, int ie, Sums64 &out,
+                                              bool half_last = false) {
+  if (ie <= ib) return false;
   constexpr int G = kGroup2;
   const double m2v = -2.0 * v, vh = v * h;
   const double tb = fma((double)ib, h, t0);
@@ -565,11 +573,13 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
   }
   double xp = XpG, xm = XmG, qq = qG;
   const double tr = fma(md, h, t0);
+  const bool half_rem = BLK_HALF_IN_REM && half_last && m < ie;
 #pragma unroll 1
   for (; m < ie; ++m) {                             // remainder, one node at a time
     const double t = fma((double)m - md, h, tr);
     const double X = xp + xm;
-    const double E = exp_tab<false>(fma(v, t, -s_mid) - X);
+    double E = exp_tab<false>(fma(v, t, -s_mid) - X);
+    if (half_rem && m == ie - 1) E *= 0.5;           // node n: weight 1/2
     v2_accumulate<DV, DX, HESS>(E, qq, X, t, S0, S1, S2, S11, S22, S12);
     xp = fma(xp, u1, xp); xm = fma(xm, u1i, xm); qq *= eq1;
   }
@@ -582,6 +592,7 @@ __device__ __forceinline__ void nodes_fp64_v2(double v, double x, double t0, dou
     out.S22 += (S22 * rx) * rx;
     out.S12 += S12 * rx;
   }
+  return half_rem;
 }
 
 // Half of the last node's contributions, evaluated in FP32: that node sits
@@ -643,9 +654,11 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
   Sums64 s{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double s_mid = shift + kLn2;                 // E = exp(vt - x cosh t - s_mid)
   (void)tab;
+  const bool own_n = mb < me && me == n + 1;
+  bool n_done = false;
 #ifndef BLK_QUAD_V1
   if (!CLAMP && !(v > 0.0 && v * fma((double)n, h, t0) < 1e-3))
-    nodes_fp64_v2<DV, DX, HESS>(v, x, t0, h, s_mid, mb, me, s);
+    n_done = nodes_fp64_v2<DV, DX, HESS>(v, x, t0, h, s_mid, mb, me, s, own_n);
   else
 #endif
     nodes_fp64<DV, DX, HESS, CLAMP>(v, x, t0, h, s_mid, mb, me, s);
@@ -653,7 +666,7 @@ __device__ __forceinline__ Sums64 quad_f64(double v, double x, double t0, double
   // returns the outer end, R1), so its term is < 2^-52 of the peak term.
   // (Leaving node n out altogether from 64 bins, as the FP32 loop does,
   // measured 0.4% slower here: profiles/r02v_skipn.log.)
-  if (mb < me && me == n + 1) {
+  if (own_n && !n_done) {
     if (n >= kEndF32MinBins) end_half_f32<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
     else end_half_f64<DV, DX, HESS>(v, x, s_mid, fma((double)n, h, t0), s);
   }
