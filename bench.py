@@ -451,6 +451,15 @@ def main():
                 "mufu_frac": counts["mufu_per_element"] * rate / mufu_ops if counts else None,
                 "peak_source": "in-run FFMA/DFMA/MUFU.EX2 microbenchmarks"}
     roof.update(common)
+    # issue slots: warp instructions per element (ncu) against 4 per clock per SM at the
+    # SM clock sampled during the timed region -- the resource the FP32 kernel is bound by
+    # (no single pipe saturates there), and a cross-check of ncu's issue-active figure
+    sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    if counts and counts.get("warp_inst_per_32_elements"):
+        wi = counts["warp_inst_per_32_elements"] / 32.0 * rate
+        roof["issue"] = {"warp_inst_per_32_elements": counts["warp_inst_per_32_elements"],
+                         "achieved_warp_inst_per_s": wi, "peak_warp_inst_per_s": 148 * 4 * sm_hz,
+                         "frac": wi / (148 * 4 * sm_hz)}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -49,5 +49,6 @@ def test_gpu_arm_contract():
         assert k in roof, k
     assert roof["stale"] is False, "profiles/roofline_counts.json is not from the current sources"
     assert 0.2 < roof["frac"] < 1.0 and 0.2 < roof["fp64_issue"]["frac"] < 1.0
+    assert 0.2 < roof["issue"]["frac"] < 1.0
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 2 * 8 * (1 << 24)
     assert "sm_mhz" in line["clocks"]
