@@ -72,7 +72,7 @@ typedef enum {
 #define BLK_MAX_NBINS 65536
 
 /* Range-finding precision (options.range_mode). */
-#define BLK_RANGE_AUTO 0  /* FP32 (FMA + MUFU pipes) when nbins >= 64 and the element is
+#define BLK_RANGE_AUTO 0  /* FP32 (FMA + MUFU pipes) when nbins >= 48 and the element is
                              inside the FP32-safe domain (x in [1e-30, 1e4], |v| <= 1e4),
                              else FP64 as below: coarse grids are sensitive to the
                              node placement (R20) */

@@ -79,7 +79,7 @@ __device__ __forceinline__ void lane_bins(int n, int sub, int &mb, int &me) {
 #endif
 // a2-a5 for one canonical element (v >= 0, x > 0 finite) of the FP64 entry
 // point: the range finder BLK_RANGE_AUTO / BLK_RANGE_F64 selects (FP32 from
-// 64 bins inside its domain, else FP64 with the table exp, which needs
+// 48 bins inside its domain, else FP64 with the table exp, which needs
 // g_exp_tab loaded), t_p, g(t_p), [t0, t1] and dmin.  Returns whether the plan
 // is usable.  Shared by the fused kernels and the plan export, so
 // bessel_logk_plan_f64 reports exactly the plan the quadrature uses.

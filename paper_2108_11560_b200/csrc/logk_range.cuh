@@ -14,7 +14,7 @@
 //     Newton point) are independent, so they run as packed f32x2 operations
 //     (FFMA2/FADD2/FMUL2, sm_100) -- half the issue slots.  The plan only has
 //     to be conservative at the log-eps level (R20), so finding it
-//     in FP32 leaves the FP64 pipe to the quadrature.  Used from 64 bins (the
+//     in FP32 leaves the FP64 pipe to the quadrature.  Used from 48 bins (the
 //     FP32 entry point: from 16) inside its safe domain.
 //   * PlanF64 / PlanF64Tab: double -- the paper's working-precision variant
 //     with Alg. 1 as printed, stopping only once converged (the oracle's
@@ -196,13 +196,13 @@ __device__ __forceinline__ void fz_update(T mid, T tn, T Fm, T dFm, T Ft, T dFt,
 //     is F(a)^2 / (2 |F'(a)|), and the search stops once it is below
 //     peak_gap.  (A relative criterion on t_p would leave gaps of
 //     |g''| (tol t_p)^2 / 2 -- over 100 for x ~ 1e-30 and v ~ 1e4.)
-// The tolerances follow the grid (the FP32 finder only runs from 64 bins,
+// The tolerances follow the grid (the FP32 finder only runs from 48 bins,
 // kF32PlanMinBins).  From 128 bins the FP64 trapezoid is insensitive to the
 // range -- widening the ends by 50% changes no output beyond 7e-14 (SURVEY
 // A.4) -- so end_nats = 8, peak_gap = 4 (the ends then lie at most ~12 nats
 // beyond the eps level, ~1/3 of the half-width): c3 +4.6%, c2 +3.9%, c5 +2.8%
 // against the relative 2^-8 rule, outputs unchanged to rounding
-// (profiles/r02g_endnats.log, profiles/r02t_e8.log); 64-127 bins can still
+// (profiles/r02g_endnats.log, profiles/r02t_e8.log); 48-127 bins can still
 // carry a discretisation error on extreme inputs that a wider range shifts,
 // so 0.1 and 1/64.  The FP32 entry point's threshold is eps = 2^-23 (R9), an
 // eps-support about half as wide, over which 64 nodes leave the trapezoid far
@@ -569,8 +569,17 @@ __device__ __forceinline__ bool valid_input(double v, double x) {
 // Below this many bins BLK_RANGE_AUTO also takes the FP64 range finder: a
 // coarse grid's discretisation error depends on where the nodes fall, so
 // only the paper's working-precision ranges reproduce the oracle there
-// (R20); from it on the result is insensitive to the range.
-constexpr int kF32PlanMinBins = 64;
+// (R20); from it on the grid has converged (n = 48
+// within 2.4e-15 / 2.1e-14 of mpmath on every config) and the result is
+// insensitive to the range: with the FP32 finder at 48-63 bins every config
+// stays within 0.05 of the north_star tolerance of the oracle element by
+// element, as the FP64 finder does, and runs 6x faster (48 bins: 1.16e10
+// against 1.85e9 evals/s on c3; at 32 bins c1 and c4 would not converge --
+// profiles/r02zt_coarse_auto.log).
+#ifndef BLK_F32_PLAN_MIN_BINS
+#define BLK_F32_PLAN_MIN_BINS 48
+#endif
+constexpr int kF32PlanMinBins = BLK_F32_PLAN_MIN_BINS;
 
 // The range finder BLK_RANGE_AUTO picks for one element.
 __device__ __forceinline__ bool use_f32_plan(int range_mode, int nbins, double v, double x) {

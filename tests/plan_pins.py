@@ -95,7 +95,7 @@ def plan_violations(v, x, plan, exact):
 
 
 def plan_check_f32(v, x, plan, exact, end_nats, peak_gap):
-    """The FP32 range finder's plan (BLK_RANGE_AUTO from 64 bins): Alg. 1-2 in
+    """The FP32 range finder's plan (BLK_RANGE_AUTO from 48 bins): Alg. 1-2 in
     FP32, FindZero ending on the paper's "until" clause at working
     tolerances in log units (R4) -- an end once F(a) >= -end_nats, the peak
     once Newton's estimate of the gap below the maximum F^2/(2|F'|) is below

@@ -66,7 +66,9 @@ def test_parity_lanes_per_element(lanes):
                   f"f32 lanes={lanes}")
 
 
-NBINS_ALL = [2, 3, 8, 16, 17, 32, 47, 48, 63, 64, 96, 127, 256, 1000]
+NBINS_ALL = [2, 3, 8, 16, 17, 32, 47, 48, 56, 63, 64, 96, 127, 256, 1000]
+# BLK_RANGE_AUTO's switch to the FP32 range finder (logk_range.cuh kF32PlanMinBins)
+F32_PLAN_MIN_BINS = 48
 
 
 def gpu_plan(v, x, nbins, range_mode=0):
@@ -116,7 +118,7 @@ def check_on_plan(got, v, x, nbins, ctx, range_mode=0, pin=60, tol_d=None):
     idx = np.unique(np.concatenate([diff[:pin], rng.choice(np.nonzero(fin)[0], min(pin, fin.sum()),
                                                            replace=False)]))
     exact = [mp_plan(v[i], x[i]) for i in idx]
-    f32 = range_mode == 0 and nbins >= 64
+    f32 = range_mode == 0 and nbins >= F32_PLAN_MIN_BINS
     if f32:   # the FP32 finder's tolerances (logk_range.cuh fz_tol_for)
         end_nats, peak_gap = (8.0, 4.0) if nbins >= 128 else (0.1, 1.0 / 64)
         bad = plan_check_f32(np.abs(v[idx]), x[idx], plan[idx], exact, end_nats, peak_gap)
@@ -129,7 +131,7 @@ def check_on_plan(got, v, x, nbins, ctx, range_mode=0, pin=60, tol_d=None):
 @pytest.mark.parametrize("nbins", NBINS_ALL)
 def test_parity_nbins(nbins):
     """Every bin count, coarse ones included, in the default (AUTO) mode.
-    From 64 bins the trapezoid error is at rounding level and any
+    From 48 bins the trapezoid error is at rounding level and any
     conservative range gives the oracle's values: element-by-element parity
     at the north_star tolerance.  Coarser grids' discretisation error depends
     on where the nodes fall, i.e. on the range, and the paper's 10-iteration
@@ -142,7 +144,7 @@ def test_parity_nbins(nbins):
     what is unique (Eq. (int) on the kernel's range) and checks the range."""
     v, x = workloads.generate("c1", 0, 1500)
     got = run_gpu(v, x, nbins=nbins)
-    if nbins >= 64:
+    if nbins >= F32_PLAN_MIN_BINS:
         assert_parity(got, run_oracle(v, x, nbins=nbins), "f64", f"nbins={nbins}")
     frac = check_on_plan(got, v, x, nbins, f"nbins={nbins}")
     print(f"nbins={nbins}: plans differing from the oracle's on {frac:.2%} of elements")
@@ -678,11 +680,11 @@ def test_wide_domain_fuzz_variants(lanes, kernel, nbins):
     _assert_wide(run_gpu(v, x, nbins=nbins, lanes_per_element=lanes, kernel=kernel), v, x, nbins)
 
 
-@pytest.mark.parametrize("lanes,nbins", [(1, 64), (4, 96), (1, 127)])
-def test_wide_domain_auto_64_127(lanes, nbins):
-    """AUTO at 64-127 bins (the FP32 range finder, 2^-10 tolerance tier) on
+@pytest.mark.parametrize("lanes,nbins", [(1, 48), (8, 56), (1, 64), (4, 96), (1, 127)])
+def test_wide_domain_auto_48_127(lanes, nbins):
+    """AUTO at 48-127 bins (the FP32 range finder, 0.1-nat tolerance tier) on
     the wide domain: small v with tiny x puts t_p ~ 25 with ranges ~30 wide,
-    where 64 nodes still leave a discretisation error that depends on the
+    where 48-127 nodes still leave a discretisation error that depends on the
     range, so the outputs are checked on the kernel's own (valid) plan."""
     v, x = _wide_inputs(5151 + nbins)
     got = run_gpu(v, x, nbins=nbins, lanes_per_element=lanes)

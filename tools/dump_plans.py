@@ -24,7 +24,7 @@ def main():
     dev = torch.device("cuda:0")
     sets = {"c1": workloads.generate("c1", 0, 1500)}
     for nb in (64, 96, 127, 2, 8):
-        sets[f"wide{nb}"] = wide((5151 if nb >= 64 else 4242) + nb)
+        sets[f"wide{nb}"] = wide((5151 if nb >= 48 else 4242) + nb)
     out = {}
     for name, (v, x) in sets.items():
         vt = torch.from_numpy(np.asarray(v, np.float64)).to(dev)
