@@ -263,6 +263,9 @@ logk_plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ 
   if (t1_out) t1_out[i] = ok ? t1 : nanv;
 }
 
+#ifndef BLK_F32_EPT
+#define BLK_F32_EPT 2   // FP32 kernel: elements per thread (2: +0.9% on c4, profiles/r02zv_f32_ept.log)
+#endif
 #ifndef BLK_F32_MINB
 // FP32 entry point: 5 resident blocks per SM (96 registers; the v3 loop
 // spills at 6 blocks / 80 registers: c4 -4%, profiles/r02e_f32v3.log)
@@ -338,6 +341,24 @@ logk_f32_kernel(const float *__restrict__ vin, const float *__restrict__ xin, si
       if (LOGK) logk[i] = o0;
       if (DV) dlogk_dv[i] = o1;
       if (DX) dlogk_dx[i] = o2;
+    }
+  } else if (BLK_F32_EPT > 1 && LPE == 1) {
+    // BLK_F32_EPT elements per thread, each next one's inputs loaded before the
+    // current one is computed (their load latency hidden behind that work)
+    size_t j = (size_t)blockIdx.x * blockDim.x * BLK_F32_EPT + threadIdx.x;
+    float vn = 1.0f, xn = 1.0f;
+    if (j < n_el) { vn = vin[j]; xn = xin[j]; }
+#pragma unroll 1
+    for (int e = 0; e < BLK_F32_EPT; ++e, j += blockDim.x) {
+      const float vc = vn, xc = xn;
+      if (e + 1 < BLK_F32_EPT && j + blockDim.x < n_el) { vn = vin[j + blockDim.x]; xn = xin[j + blockDim.x]; }
+      float o0, o1, o2;
+      f32_element<LOGK, DV, DX, 1>(vc, xc, 0, nbins, range_mode, o0, o1, o2);
+      if (j < n_el) {
+        if (LOGK) logk[j] = o0;
+        if (DV) dlogk_dv[j] = o1;
+        if (DX) dlogk_dx[j] = o2;
+      }
     }
   } else {
     if (live) { vraw = vin[i]; x = xin[i]; }
@@ -473,7 +494,9 @@ template <class K, class T>
 blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, const T *v,
                     const T *x, T *a, T *b, T *c, int nbins, int mode) {
   const size_t total = n * (size_t)lanes;
-  const size_t blocks = (total + threads - 1) / threads;
+  // FP32 kernel, one element per lane, BLK_F32_EPT2: two elements per thread
+  const size_t per_block = (size_t)threads * ((sizeof(T) == 4 && lanes == 1) ? BLK_F32_EPT : 1);
+  const size_t blocks = (total + per_block - 1) / per_block;
   if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "grid too large");
 #ifdef BLK_SMEM_PAD
   // tuning builds only: pad dynamic shared memory to cap resident blocks per SM
