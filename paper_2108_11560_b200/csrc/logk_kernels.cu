@@ -492,10 +492,11 @@ blk_status validate(const T *v, const T *x, size_t n, const void *o1, const void
 
 template <class K, class T>
 blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, const T *v,
-                    const T *x, T *a, T *b, T *c, int nbins, int mode) {
+                    const T *x, T *a, T *b, T *c, int nbins, int mode, int ept = 1) {
   const size_t total = n * (size_t)lanes;
-  // FP32 kernel, one element per lane, BLK_F32_EPT2: two elements per thread
-  const size_t per_block = (size_t)threads * ((sizeof(T) == 4 && lanes == 1) ? BLK_F32_EPT : 1);
+  // ept: elements per thread (the scalar-I/O FP32 kernel at one element per
+  // lane: BLK_F32_EPT; every other kernel 1)
+  const size_t per_block = (size_t)threads * (size_t)ept;
   const size_t blocks = (total + per_block - 1) / per_block;
   if (blocks > 0x7fffffffULL) return fail(BLK_EINVAL, "grid too large");
 #ifdef BLK_SMEM_PAD
@@ -510,16 +511,18 @@ blk_status launch_k(K kern, size_t n, int lanes, int threads, cudaStream_t st, c
   return BLK_OK;
 }
 
+// elements per thread of the one-element-per-lane scalar-I/O kernel (FP32: BLK_F32_EPT)
+#define BLK_EPT_OF(ptr) (sizeof(*(ptr)) == 4 ? BLK_F32_EPT : 1)
 #ifdef BLK_MIN_INSTANCES
 // tuning-variant builds (tools/build_variants.py): one element per lane only
 #define BLK_DISPATCH_LPE(KER, L, O1, O2, O3) \
   if (vec) return launch_k(KER<O1, O2, O3, 1, true>, n, 1, th, stream, v, x, a, b, c, nbins, mode); \
-  return launch_k(KER<O1, O2, O3, 1>, n, 1, th, stream, v, x, a, b, c, nbins, mode);
+  return launch_k(KER<O1, O2, O3, 1>, n, 1, th, stream, v, x, a, b, c, nbins, mode, BLK_EPT_OF(v));
 #else
 #define BLK_DISPATCH_LPE(KER, L, O1, O2, O3)                                        \
   if (vec) return launch_k(KER<O1, O2, O3, 1, true>, n, 1, th, stream, v, x, a, b, c, nbins, mode); \
   switch (L) {                                                                      \
-    case 1: return launch_k(KER<O1, O2, O3, 1>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
+    case 1: return launch_k(KER<O1, O2, O3, 1>, n, L, th, stream, v, x, a, b, c, nbins, mode, BLK_EPT_OF(v)); \
     case 2: return launch_k(KER<O1, O2, O3, 2>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
     case 4: return launch_k(KER<O1, O2, O3, 4>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
     case 8: return launch_k(KER<O1, O2, O3, 8>, n, L, th, stream, v, x, a, b, c, nbins, mode); \
