@@ -265,6 +265,9 @@ __device__ __forceinline__ double exp_cw(double a) {
   return fma(ts, exp_em1(r), ts);
 }
 
+#ifndef BLK_PLAN_LOG_TAB
+#define BLK_PLAN_LOG_TAB 1
+#endif
 // FP64 range-finder point evaluations with the table exp and rcp64 instead
 // of libdevice exp and IEEE division (kernels that load the exp table):
 // 3-4x fewer instructions per evaluation, ~1 ulp like the libm calls.
@@ -292,13 +295,23 @@ struct PlanF64Tab {
   __device__ __forceinline__ void thr(double c, double t, double &F, double &dF) const {
     double e, ei, q, r;
     parts(t, e, ei, q, r);
-    F = v * t + log1p(q) - hx * (e + ei) - c;
+    F = v * t + log1p_q(q) - hx * (e + ei) - c;
     dF = v * ((1.0 - q) * r) - hx * (e - ei);
   }
   __device__ __forceinline__ double gval(double t) const {
     double e, ei;
     ep(t, e, ei);
-    return v * t + log1p(exp_cw(fmax(m2v * t, -707.0))) - kLn2 - hx * (e + ei);
+    return v * t + log1p_q(exp_cw(fmax(m2v * t, -707.0))) - kLn2 - hx * (e + ei);
+  }
+  // log(1 + q) for q = e^{-2vt} in [0, 1]: the table log of 1 + q, absolute
+  // error < 4e-16 (the rounding of 1 + q included) -- F's other terms carry
+  // at least that much -- against ~30 instructions of libdevice log1p
+  __device__ __forceinline__ static double log1p_q(double q) {
+#if BLK_PLAN_LOG_TAB
+    return log_tab(1.0 + q);
+#else
+    return log1p(q);
+#endif
   }
 };
 __device__ __forceinline__ Plan<double> make_plan_f64_tab(double v, double x, double log_eps) {
