@@ -40,10 +40,14 @@ constexpr int kAnchor = BLK_ANCHOR; // v1 loop: FP64 re-anchoring interval for e
 #define BLK_GROUP 4
 #endif
 #ifndef BLK_MINB
-// __launch_bounds__ min blocks per SM: 5 lets ptxas use 90 registers (6 capped
-// it at 78 and cost the session-3 loop 2-2.5%; 4 measures the same as 5 on
-// c2/c3/c5, profiles/r01s3g_minb_sweep.log)
-#define BLK_MINB 5
+// __launch_bounds__ min blocks per SM: 4 (112 registers, 16 warps/SM).  The v2
+// loop with each group's cosh factors formed from the group base (BLK_X_DIRECT)
+// needs the room: at 5 blocks (<= 102 registers) ptxas re-schedules it to 102
+// instructions (-5%), at 4 it is 94 instructions with 167 operand-read cycles
+// per 4 nodes instead of 97 / 174: c3 +2.9%, c5 +2.7%, c2 +2.3%
+// (profiles/r02zzg_xdirect*.log).  (Round 1: 6 capped it at 78 registers and
+// cost 2-2.5%; without BLK_X_DIRECT 4 and 5 measure the same.)
+#define BLK_MINB 4
 #endif
 constexpr int kGroup = BLK_GROUP; // nodes evaluated together (independent exp chains)
 #ifndef BLK_GROUP2
@@ -54,6 +58,13 @@ constexpr int kGroup2 = BLK_GROUP2; // v2 loop group size
 #define BLK_V2_UNROLL 1
 #endif
 constexpr int kV2Unroll = BLK_V2_UNROLL; // tuning knob: unroll of the v2 group loop
+#ifndef BLK_X_DIRECT
+// v2 loop: X_j = x cosh t_j of the group's nodes j = 1..3 as Xp_c e^{jh} + Xm_c
+// e^{-jh} from the group base (one FMUL + one FMA, no chain through the group)
+// instead of the Xp, Xm recurrences plus a sum: 3 FP64 instructions and 7
+// operand-read cycles fewer per group (BLK_MINB)
+#define BLK_X_DIRECT 1
+#endif
 #ifndef BLK_S1_SPLIT
 #define BLK_S1_SPLIT 1
 #endif
@@ -522,6 +533,12 @@ __device__ __forceinline__ bool nodes_fp64_v2(double v, double x, double t0, dou
   // e^{-2v G h} by squaring: q only enters w = E (1 + q), where a few ulp of
   // drift over n/G steps are far below the other rounding (measured +1%)
   const double eq2 = eq1 * eq1, eqG = eq2 * eq2;
+#if BLK_X_DIRECT
+  // e^{+-jh}, j = 1..3: X_j = Xp_c e^{jh} + Xm_c e^{-jh} from the group base
+  // (one rounding each, no chain inside the group)
+  const double ej1 = 1.0 + u1, ej2 = ej1 * ej1, ej3 = ej2 * ej1;
+  const double ei1 = 1.0 + u1i, ei2 = ei1 * ei1, ei3 = ei2 * ei1;
+#endif
   double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0, S1j = 0.0;
   if (ib == 0) {
     // node 0 carries weight 1/2: take half of it back (exact state)
@@ -538,6 +555,18 @@ __device__ __forceinline__ bool nodes_fp64_v2(double v, double x, double t0, dou
     const double Bc = fma(v, tc, -s_mid);
     double X[G], a[G], q[G], kd[G], r[G], ts[G];
     int k[G];
+#if BLK_X_DIRECT
+    double qq = qG;
+    X[0] = XpG + XmG;
+    X[1] = fma(XpG, ej1, XmG * ei1);
+    X[2] = fma(XpG, ej2, XmG * ei2);
+    X[3] = fma(XpG, ej3, XmG * ei3);
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      q[j] = qq;
+      if (j + 1 < G) qq *= eq1;
+    }
+#else
     double xp = XpG, xm = XmG, qq = qG;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
@@ -545,6 +574,7 @@ __device__ __forceinline__ bool nodes_fp64_v2(double v, double x, double t0, dou
       q[j] = qq;
       if (j + 1 < G) { xp = fma(xp, u1, xp); xm = fma(xm, u1i, xm); qq *= eq1; }
     }
+#endif
     XpG = fma(XpG, uG, XpG); XmG = fma(XmG, uGi, XmG); qG *= eqG;
 #pragma unroll
     for (int j = 0; j < G; ++j) a[j] = (j == 0 ? Bc : fma(double(j), vh, Bc)) - X[j];
