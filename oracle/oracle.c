@@ -141,6 +141,10 @@ static double find_zero(const oracle_ctx *c, ofun F, ofun dF, double a, double b
     return a;
 }
 
+/* DESIGN.md R23: ranges must end below t = 709 (e^t overflows double at
+ * 709.78, cosh t at 710.48). */
+static const double kTMax = 709.0;
+
 /* Integration plan of Alg. 3 for one canonical (v >= 0, x > 0). */
 static int oracle_plan(oracle_ctx *c, int max_iter, double tol,
                        double *tp_out, double *t0_out, double *t1_out)
@@ -159,6 +163,12 @@ static int oracle_plan(oracle_ctx *c, int max_iter, double tol,
     if (find_range(c, dfun, tp, &lo, &hi) != 0)         /* P:266 */
         return -1;
     double t1 = find_zero(c, dfun, g1, hi, lo, max_iter, tol); /* P:267 */
+    /* DESIGN.md R23: an eps-support that reaches t ~ 709, where e^t and
+     * cosh t overflow in double, cannot be integrated by the method in double
+     * (g is -inf there although the integrand is not small: x below ~1e-306
+     * for small orders) -- no result, like an invalid input (R16). */
+    if (!(t1 < kTMax))
+        return -1;
     *tp_out = tp;
     *t0_out = t0;
     *t1_out = t1;

@@ -96,7 +96,10 @@ __device__ __forceinline__ bool element_plan_f64(double v, double x, int nbins, 
     const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
     ok = p.ok; tp = p.tp; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
   }
-  return ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+  // R23: a range reaching t = kTMax (709; e^t overflows at 709.78) cannot be
+  // integrated in double -- no result, as in the oracle (the FP32 finder's
+  // domain, x >= 1e-30, keeps t1 far below it)
+  return ok && isfinite(t1) && isfinite(gp) && t1 > t0 && t1 < kTMax;
 }
 
 // One element (or one lane of LPE) of the FP64 path after the exp table is

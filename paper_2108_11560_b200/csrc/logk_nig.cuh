@@ -58,7 +58,7 @@ nig_f64_kernel(const double *__restrict__ y, size_t n, double a, double b, doubl
         const Plan<double> p = make_plan_f64_tab(1.0, z, kLogEpsF64);
         ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
       }
-      ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+      ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0 && t1 < kTMax;   // R23
       if (ok) {
         const double h = (t1 - t0) * rcp64((double)nbins);
         const Sums64 s = dmin > -600.0

@@ -536,7 +536,9 @@ __device__ __forceinline__ bool nodes_fp64_v2(double v, double x, double t0, dou
 #if BLK_X_DIRECT
   // e^{+-jh}, j = 1..3: X_j = Xp_c e^{jh} + Xm_c e^{-jh} from the group base
   // (one rounding each, no chain inside the group)
-  const double ej1 = 1.0 + u1, ej2 = ej1 * ej1, ej3 = ej2 * ej1;
+  // (capped like u1: a coarse grid's e^{2h} may pass DBL_MAX; 0 * inf must not
+  // turn an underflowed X+ into NaN)
+  const double ej1 = 1.0 + u1, ej2 = fmin(ej1 * ej1, 8e307), ej3 = fmin(ej2 * ej1, 8e307);
   const double ei1 = 1.0 + u1i, ei2 = ei1 * ei1, ei3 = ei2 * ei1;
 #endif
   double S0 = 0.0, S1 = 0.0, S2 = 0.0, S11 = 0.0, S22 = 0.0, S12 = 0.0, S1j = 0.0;

@@ -566,6 +566,11 @@ __device__ __forceinline__ bool valid_input(double v, double x) {
   return xb > 0 && xb < 0x7FF0000000000000LL && (vb & 0x7FFFFFFFFFFFFFFFLL) < 0x7FF0000000000000LL;
 }
 
+// DESIGN.md R23: ranges must end below t = 709 (e^t overflows double at
+// 709.78, cosh t at 710.48); beyond, the element has no result (NaN), in the
+// oracle as in the kernels.
+constexpr double kTMax = 709.0;
+
 // Below this many bins BLK_RANGE_AUTO also takes the FP64 range finder: a
 // coarse grid's discretisation error depends on where the nodes fall, so
 // only the paper's working-precision ranges reproduce the oracle there

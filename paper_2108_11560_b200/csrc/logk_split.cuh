@@ -36,7 +36,7 @@ plan_f64_kernel(const double *__restrict__ vin, const double *__restrict__ xin, 
       const Plan<double> p = make_plan_f64_tab(v, x, kLogEpsF64);
       ok = p.ok; t0 = p.t0; t1 = p.t1; gp = p.gp; dmin = p.dmin;
     }
-    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0;
+    ok = ok && isfinite(t1) && isfinite(gp) && t1 > t0 && t1 < kTMax;   // as element_plan_f64 (R23)
   }
   PlanRec r;
   r.t0 = t0; r.h = (t1 - t0) * rcp64((double)nbins); r.gp = gp;

@@ -623,6 +623,30 @@ def test_f64_far_out_extremes():
     assert np.all(errors(got["dv"][ok], dv[ok], "dv") <= tol_d[ok])
 
 
+def test_ranges_past_double_overflow_are_nan():
+    """R23: an eps-support that reaches t = 709 (e^t overflows double at 709.78,
+    cosh t at 710.48 -- x near or below DBL_MIN for small orders, where the
+    integrand is still O(1) there) has no result in double, on the GPU as in
+    the oracle: NaN on both sides, at every bin count and in both range modes;
+    x = 1e-300 (ranges ending at ~695) stays finite and in parity."""
+    xs = [5e-324, 1e-320, 1e-310, 2.2e-308, 1e-306, 1e-303, 1e-300]
+    vs = [0.0, 0.5, 1.0, 3.0]
+    v = np.array([a for a in vs for _ in xs])
+    x = np.array([b for _ in vs for b in xs])
+    for nb in (3, 48, 128):
+        for mode in (blk.BLK_RANGE_AUTO, blk.BLK_RANGE_F64):
+            got = run_gpu(v, x, nbins=nb, range_mode=mode)
+            lk, dv, dx, plan = oracle.logk(v, x, nb, with_plan=True)
+            for k, r in zip(KINDS, (lk, dv, dx)):
+                assert np.array_equal(np.isnan(got[k]), np.isnan(r)), (nb, mode, k)
+            fin = ~np.isnan(lk)
+            assert np.all(plan[fin, 3] < 709.0) and fin[x == 1e-300].all()
+            if nb >= F32_PLAN_MIN_BINS:
+                assert_parity({k: g[fin] for k, g in got.items()},
+                              {k: r[fin] for k, r in zip(KINDS, (lk, dv, dx))}, "f64",
+                              f"nbins={nb} mode={mode}")
+
+
 def test_hessian_wide_fuzz():
     """Second derivatives beyond the configs: v in {0} U logU[1e-3, 1e3], x in
     logU[1e-6, 1e4]; bound as in test_parity_hessian, widened by the

@@ -473,3 +473,19 @@ def test_plan_pin_rejects_stalled_findzero(plan_samples, max_iter):
     for cfg, (v, x, ex) in plan_samples.items():
         *_, plan = oracle.logk(v, x, with_plan=True, max_iter=max_iter)
         assert plan_violations(v, x, plan, ex).any(), (cfg, max_iter)
+
+
+def test_reading_R23_ranges_past_double_overflow():
+    """R23: where the eps-support reaches t = 709 the method cannot evaluate its
+    integrand in double (cosh t overflows at 710.48 while x cosh t is still
+    O(1)): the oracle returns NaN (like an invalid input, R16) instead of a
+    silently truncated integral.  Closed form K_{1/2}(x) = sqrt(pi/(2x)) e^{-x}:
+    at x = 1e-300 (support ending near t = 695) the oracle is finite and
+    matches it; at x = 1e-310 it would need t up to ~717."""
+    v = np.array([0.5, 0.5, 0.0, 1.0])
+    x = np.array([1e-300, 1e-310, 5e-324, 2.2e-308])
+    lk, dv, dx, plan = oracle.logk(v, x, 512, with_plan=True)
+    assert np.isfinite(lk[0]) and plan[0, 3] < 709.0
+    ref = 0.5 * np.log(np.pi / (2.0 * x[0])) - x[0]
+    assert abs(lk[0] - ref) <= 1e-12 * abs(ref)
+    assert np.isnan(lk[1:]).all() and np.isnan(dv[1:]).all() and np.isnan(dx[1:]).all()
