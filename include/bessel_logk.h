@@ -28,7 +28,10 @@
  *   - Per-element domain (never fails the batch): x <= 0, x or v NaN/inf ->
  *     all requested outputs NaN.  v < 0 -> evaluated at |v| with dlogk_dv
  *     negated (K is even in v).  The FindRange doubling cap (t <= t_s + 2^12)
- *     exceeded -> NaN.
+ *     exceeded -> NaN.  FP64 entry points: an integration range reaching
+ *     t = 709 (e^t overflows double; x near or below DBL_MIN for small orders)
+ *     -> NaN, as in the oracle (R23).  Meaningful derivatives need
+ *     eps (x + v t_p) << 1 (R22).
  *   - Results are a pure function of (v[i], x[i], nbins, entry point,
  *     options, lanes per element): bit-identical across runs, batch
  *     permutations, shard counts and output subsets.  (lanes_per_element = 0
